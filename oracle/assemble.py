@@ -1,0 +1,216 @@
+"""Oracle assembly of the multicontinuum block system  M dp/dt + A p = F,  A = D + Q.
+
+TEST INFRASTRUCTURE ONLY (see oracle/__init__.py).
+
+Follows PAPER.md §3.1:
+  * Eq. app-md: TPFA  sum_j T_ij (p_i - p_j), T = k|E|/d
+    (PAPER.md:266-267), storage c|cell|, transfer
+    sigma_il (p_m,i - p_f,l).
+  * Eq. app-tc: co-located sigma_12,ii.
+  * Eq. app-mc: block matrices
+        M = diag(M_a),   m_a,ii = c_a,i |cell_i|
+        D = diag(D_a),   a_ii = sum_n T_in,  a_ij = -T_ij
+        Q: diagonal blocks sum_{b!=a} Q_ab (as the diagonal of row sums),
+           off-diagonal blocks -Q_ab,  Q_ba = Q_ab^T
+  * NLMC coarse system Eq. app-nlmc with M = c|K|.
+
+Readings:
+  C1  |cell| = h^2 (h = 1/n), fracture cell |iota| = h;
+  C2  heterogeneous k: T_face = 2 k_i k_j / (k_i + k_j)  (|E|/d = 1); constant k: T = k;
+  C3  Dirichlet on the left/right edge: half-cell face T_b = 2 k_i on the diagonal, T_b g in F;
+  C6  embedded Q entry (host(l), l) = given per-fracture-cell sigma;
+  C7  fracture T_f = k_f / h between consecutive fracture cells;
+  C9  co-located Q_ii = sigma_12 h^2;
+  C11 NLMC mass m = c (unit coarse measure);
+  C12 NLMC Dirichlet DOFs become identity rows (m = 0, F = g, u0 = g), their
+      columns eliminated into F of the free rows, free rows keep their diagonal.
+"""
+from __future__ import annotations
+
+import numpy as np
+import scipy.sparse as sp
+
+
+class System:
+    """Assembled block system: sizes per continuum, M (vector), A (CSR), F, u0."""
+
+    def __init__(self, sizes, M, A, F, u0, names):
+        self.sizes = list(sizes)
+        self.offsets = np.concatenate([[0], np.cumsum(self.sizes)]).astype(np.int64)
+        self.M = np.asarray(M, dtype=np.float64)
+        self.A = sp.csr_matrix(A)
+        self.F = np.asarray(F, dtype=np.float64)
+        self.u0 = np.asarray(u0, dtype=np.float64)
+        self.names = list(names)
+
+    @property
+    def L(self):
+        return len(self.sizes)
+
+    def block(self, a):
+        return slice(int(self.offsets[a]), int(self.offsets[a + 1]))
+
+    def split(self, u):
+        return [u[self.block(a)] for a in range(self.L)]
+
+
+def laplacian_from_edges(n, i, j, t):
+    """sum_e t_e (e_i - e_j)(e_i - e_j)^T : a_ii = sum t, a_ij = -t."""
+    i = np.asarray(i, dtype=np.int64)
+    j = np.asarray(j, dtype=np.int64)
+    t = np.asarray(t, dtype=np.float64)
+    rows = np.concatenate([i, j, i, j])
+    cols = np.concatenate([i, j, j, i])
+    vals = np.concatenate([t, t, -t, -t])
+    return sp.csr_matrix(sp.coo_matrix((vals, (rows, cols)), shape=(n, n)))
+
+
+def grid_faces(nx, ny):
+    """Interior faces of the nx x ny row-major grid (i = iy*nx + ix): (i, j) pairs."""
+    iy, ix = np.divmod(np.arange(nx * ny, dtype=np.int64), nx)
+    xm = ix < nx - 1
+    ym = iy < ny - 1
+    cell = np.arange(nx * ny, dtype=np.int64)
+    fi = np.concatenate([cell[xm], cell[ym]])
+    fj = np.concatenate([cell[xm] + 1, cell[ym] + nx])
+    return fi, fj
+
+
+def face_transmissibility(k, fi, fj):
+    """T = k |E|/d with |E|/d = h/h = 1; harmonic mean for a k field (C2)."""
+    if np.isscalar(k) or np.ndim(k) == 0:
+        return np.full(len(fi), float(k))
+    k = np.asarray(k, dtype=np.float64)
+    return 2.0 * k[fi] * k[fj] / (k[fi] + k[fj])
+
+
+def grid_continuum(nx, ny, h, k, c, dirichlet):
+    """One d-dimensional continuum on the nx x ny grid: (D, M, F) per Eq. app-md / app-mc.
+
+    dirichlet = (g_left, g_right) (either may be None = no-flow) or None: all faces
+    no-flow, the paper's homogeneous Neumann condition.
+    """
+    N = nx * ny
+    fi, fj = grid_faces(nx, ny)
+    D = laplacian_from_edges(N, fi, fj, face_transmissibility(k, fi, fj))
+    M = np.full(N, float(c) * h * h)                       # m = c |cell|, |cell| = h^2 (C1)
+    F = np.zeros(N)
+    if dirichlet is not None:
+        gL, gR = dirichlet
+        kk = np.full(N, float(k)) if np.ndim(k) == 0 else np.asarray(k, dtype=np.float64)
+        ix = np.arange(N) % nx
+        bdiag = np.zeros(N)
+        for col, g in ((0, gL), (nx - 1, gR)):
+            if g is None:
+                continue
+            cells = np.nonzero(ix == col)[0]
+            Tb = kk[cells] * h / (h / 2.0)                 # half-cell face, |E| = h, d = h/2 (C3)
+            bdiag[cells] += Tb
+            F[cells] += Tb * float(g)
+        D = D + sp.diags(bdiag)
+    return sp.csr_matrix(D), M, F
+
+
+def fracture_continuum(n, h, cells, edges, k_f, c_f):
+    """1D fracture continuum: T_f = k_f |E|/d with |E| = 1, d = h (C7); m = c_f h (C1)."""
+    Nf = len(cells)
+    e = np.asarray(edges, dtype=np.int64).reshape(-1, 2)
+    D = laplacian_from_edges(Nf, e[:, 0], e[:, 1], np.full(len(e), float(k_f) / h))
+    M = np.full(Nf, float(c_f) * h)
+    F = np.zeros(Nf)
+    return D, M, F
+
+
+def block_system(sizes, Dblocks, Mblocks, Fblocks, Qpairs, u0blocks, names):
+    """A = D + Q with Q laid out as in Eq. app-mc.
+
+    Qpairs: dict (a, b) -> sparse Q_ab (N_a x N_b), a != b, entries sigma >= 0.
+    Q_ba := Q_ab^T.  Diagonal block a gets diag(sum_b Q_ab 1).
+    """
+    L = len(sizes)
+    blocks = [[None] * L for _ in range(L)]
+    rowsum = [np.zeros(s) for s in sizes]
+    for (a, b), Q in Qpairs.items():
+        Q = sp.csr_matrix(Q)
+        rowsum[a] += np.asarray(Q.sum(axis=1)).ravel()
+        rowsum[b] += np.asarray(Q.sum(axis=0)).ravel()      # rows of Q_ba = Q_ab^T
+        blocks[a][b] = -Q
+        blocks[b][a] = -Q.T
+    for a in range(L):
+        blocks[a][a] = sp.csr_matrix(Dblocks[a]) + sp.diags(rowsum[a])
+        for b in range(L):
+            if blocks[a][b] is None:
+                blocks[a][b] = sp.csr_matrix((sizes[a], sizes[b]))
+    A = sp.bmat(blocks, format="csr")
+    return System(sizes, np.concatenate(Mblocks), A, np.concatenate(Fblocks),
+                  np.concatenate(u0blocks), names)
+
+
+def assemble_fine(scn) -> System:
+    """Fine-grid FV system of a generator scenario (kind == 'fine')."""
+    n, h = scn["n"], scn["h"]
+    sizes, Ds, Ms, Fs, names = [], [], [], [], []
+    for cont in scn["continua"]:
+        if cont["kind"] == "grid":
+            D, M, F = grid_continuum(n, n, h, cont["k"], cont["c"], cont["dirichlet"])
+        else:
+            fr = scn["fracture"]
+            D, M, F = fracture_continuum(n, h, fr["cells"], fr["edges"], cont["k"], cont["c"])
+        sizes.append(len(M))
+        Ds.append(D)
+        Ms.append(M)
+        Fs.append(F)
+        names.append(cont["name"])
+    Q = {}
+    for cp in scn["couplings"]:
+        a, b = cp["a"], cp["b"]
+        if cp["type"] == "embedded":
+            cells = scn["fracture"]["cells"]
+            sig = np.asarray(cp["sigma"], dtype=np.float64)
+            Q[(a, b)] = sp.csr_matrix((sig, (cells, np.arange(len(cells)))), shape=(sizes[a], sizes[b]))
+        elif cp["type"] == "colocated":
+            Q[(a, b)] = sp.diags(np.full(sizes[a], float(cp["sigma"]) * h * h))   # C9
+        else:
+            raise ValueError(cp["type"])
+    u0 = [np.zeros(s) for s in sizes]                        # u0 = 0 (C17)
+    return block_system(sizes, Ds, Ms, Fs, Q, u0, names)
+
+
+def assemble_nlmc(scn) -> System:
+    """NLMC-style coarse system (config 3) with Dirichlet identity rows (C11, C12)."""
+    nc = scn["nc"]
+    Nb = nc * nc
+    sizes = [Nb, Nb]
+    Ds = [laplacian_from_edges(Nb, i, j, t) for (i, j, t) in scn["within"]]
+    bi, bj, bt = scn["between"]
+    Q = {(0, 1): sp.csr_matrix((bt, (bi, bj)), shape=(Nb, Nb))}
+    Ms = [np.full(Nb, float(c)) for c in scn["c"]]           # unit coarse measure (C11)
+    Fs = [np.zeros(Nb), np.zeros(Nb)]
+    u0 = [np.zeros(Nb), np.zeros(Nb)]
+    sys = block_system(sizes, Ds, Ms, Fs, Q, u0, ["matrix", "fracture"])
+    mask = np.concatenate([scn["dirichlet"][a][0] for a in range(2)])
+    g = np.concatenate([scn["dirichlet"][a][1] for a in range(2)])
+    return apply_dirichlet_rows(sys, mask, g)
+
+
+def apply_dirichlet_rows(sys: System, mask, g) -> System:
+    """Identity rows for fixed DOFs, columns eliminated symmetrically into F (C12)."""
+    mask = np.asarray(mask, dtype=bool)
+    g = np.where(mask, np.asarray(g, dtype=np.float64), 0.0)
+    A = sp.csr_matrix(sys.A)
+    free = ~mask
+    F = sys.F - A @ g                                       # move fixed columns to the RHS
+    keep = sp.diags(free.astype(np.float64))
+    A = keep @ A @ keep + sp.diags(mask.astype(np.float64))  # zero fixed rows/cols, unit diagonal
+    F = np.where(mask, g, F)
+    M = np.where(mask, 0.0, sys.M)
+    u0 = np.where(mask, g, sys.u0)
+    return System(sys.sizes, M, A, F, u0, sys.names)
+
+
+def assemble(scn) -> System:
+    if scn["kind"] == "fine":
+        return assemble_fine(scn)
+    if scn["kind"] == "nlmc":
+        return assemble_nlmc(scn)
+    raise ValueError(scn["kind"])
