@@ -1,0 +1,197 @@
+/*
+ * mc.h — C ABI of libmc: one time step of the multicontinuum flow system
+ *
+ *     M dp/dt + A p = F,   A = D + Q                         (Eq. app-mc)
+ *
+ * advanced either by the coupled backward-Euler scheme
+ *
+ *     (M/tau + A) p^n = M/tau p^{n-1} + F                    (Eq. ct-mc)
+ *
+ * or by the decoupled D-scheme (A0 = blockdiag(A), A1 = A - A0, the inter-continuum
+ * transfer lagged to time layer n-1), one independent SPD solve per continuum:
+ *
+ *     (M_a/tau + D_a + sum_b Q_ab) p_a^n = M_a/tau p_a^{n-1} + F_a + sum_b Q_ab p_b^{n-1}
+ *                                                            (Eq. si-mc, D-scheme)
+ *
+ * Every linear system is solved on the GPU by Jacobi-preconditioned CG (the paper's
+ * solver is CG) in fp64, stopping at the first iterate whose recursive
+ * residual satisfies ||r_k||_2 <= rtol ||b||_2 (reading C13), warm-started
+ * from p^{n-1}.  All kernels are hand-written for sm_100a.
+ *
+ * Conventions
+ *  - No exceptions cross this ABI; every call returns mc_status and mc_error_string()
+ *    returns a message for the last failure on that context (continuum and step named).
+ *  - Array arguments may be HOST or DEVICE pointers (unified addressing; the library
+ *    inspects each pointer).  The library copies everything it keeps during the call,
+ *    so the caller may free its arrays as soon as the call returns.  No pointer passed
+ *    in is ever written, except the documented output arguments.
+ *  - Indices are 0-based int32; counts are int64.  fp64 everywhere.
+ *  - All device work is ordered on mc_options.stream (the caller's cudaStream_t, or the
+ *    legacy default stream when NULL).
+ *  - A context is not thread-safe; use one context per host thread.
+ */
+#ifndef MC_H
+#define MC_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define MC_ABI_VERSION 1
+#define MC_MAX_CONTINUA 4
+
+typedef struct mc_ctx mc_ctx;
+
+typedef enum {
+  MC_OK = 0,
+  MC_ERR_ARG = 1,        /* invalid argument (range, sign, CSR/index structure, sizes)      */
+  MC_ERR_STATE = 2,      /* call out of order (coupling before continuum, step before setup) */
+  MC_ERR_NOMEM = 3,      /* device or host allocation failed                                 */
+  MC_ERR_CUDA = 4,       /* a CUDA runtime call failed (message carries cudaGetErrorString)  */
+  MC_ERR_NOCONV = 5,     /* a CG solve hit maxit; the state is NOT advanced    */
+  MC_ERR_BREAKDOWN = 6   /* CG breakdown (p.q <= 0): operator not SPD                        */
+} mc_status;
+
+typedef enum {
+  MC_GRID2D = 0,  /* d-dimensional continuum on a structured nx x ny grid of h x h cells
+                     (PAPER.md:247-248), TPFA 5-point operator   */
+  MC_GRAPH = 1    /* continuum given by its cells and symmetric two-point connections:
+                     the (d-1)-dimensional fracture mesh or an
+                     NLMC coarse operator                              */
+} mc_kind;
+
+typedef enum {
+  MC_COUPLED = 0,      /* Eq. ct-mc: one CG solve over all continua per step            */
+  MC_DECOUPLED_D = 1   /* Eq. si-mc, D-scheme: one CG solve per continuum per step      */
+} mc_scheme;
+
+typedef struct {
+  double tau;        /* time step tau > 0                                     */
+  double rtol;       /* CG stop ||r_k|| <= rtol ||b||; <= 0 selects 1e-12 (BASELINE.json:5)   */
+  int64_t maxit;     /* per solve; <= 0 selects min(10 N_solve, 2e6)                          */
+  int32_t ctas;      /* persistent CTAs per step kernel; 0 = all co-resident (148 x occupancy) */
+  int32_t device;    /* CUDA device ordinal                                                    */
+  void* stream;      /* cudaStream_t for all work, NULL = legacy default stream               */
+} mc_options;
+
+/*
+ * One continuum alpha.  Storage m_i = c_i |cell_i|; source
+ * F_i = f_i |cell_i|; initial state p_alpha^0 = u0.
+ *
+ * MC_GRID2D: n = nx*ny cells, row-major (i = iy*nx + ix), |cell| = h^2.  Interior faces
+ *   carry T = k|E|/d = k (|E| = d = h); with a per-cell k field the face
+ *   value is the harmonic mean 2 k_i k_j / (k_i + k_j) (reading C2).  All outer faces
+ *   are no-flow unless bc_left / bc_right = 1: then the left
+ *   (ix = 0) / right (ix = nx-1) faces are Dirichlet faces with value g_left / g_right,
+ *   half-cell transmissibility T_b = k_i h / (h/2) = 2 k_i (reading C3).
+ * MC_GRAPH: n cells, |cell_i| = measure[i] (or measure_const); n_edges undirected
+ *   connections (edge_i[e], edge_j[e]), 0 <= i,j < n, i != j, each pair at most once,
+ *   with flux T_e (p_i - p_j).  T_e = edge_t[e] if edge_t != NULL,
+ *   else T_e = k_e * edge_geom where k_e = k_const, or the harmonic mean of k[i], k[j]
+ *   when k != NULL, and edge_geom = |E|/d.  dirichlet (optional): per cell, NaN = free,
+ *   otherwise the cell is a fixed-value DOF: identity row with m = 0, F = g, u0 = g,
+ *   and every connection / coupling touching it is eliminated into the free cell's
+ *   diagonal and F (reading C12).
+ * Scalars *_const are used when the corresponding pointer is NULL.
+ */
+typedef struct {
+  mc_kind kind;
+  int64_t n;
+  const double* c;        double c_const;        /* storage coefficient c >= 0            */
+  const double* k;        double k_const;        /* permeability k >= 0                   */
+  const double* f;                               /* volumetric source, NULL = 0           */
+  const double* u0;                              /* initial state, NULL = 0               */
+  /* MC_GRID2D */
+  int32_t nx, ny;
+  double h;                                      /* cell edge length > 0                  */
+  int32_t bc_left, bc_right;                     /* 0 = no-flow, 1 = Dirichlet            */
+  double g_left, g_right;
+  /* MC_GRAPH */
+  const double* measure;  double measure_const;  /* |cell| > 0                            */
+  int64_t n_edges;
+  const int32_t* edge_i;
+  const int32_t* edge_j;
+  const double* edge_t;                          /* explicit T_e >= 0, or NULL            */
+  double edge_geom;                              /* |E|/d when edge_t == NULL             */
+  const double* dirichlet;                       /* NULL, or per cell NaN / fixed value   */
+} mc_continuum_desc;
+
+/*
+ * Transfer between continua a != b: Q_ab has entries q_{i j} = sigma_e at
+ * (i = i_a[e], j = j_b[e]), e < nnz; Q_ba = Q_ab^T.
+ * The library adds sum_j q_ij to diagonal row i of a and sum_i q_ij to row j of b and
+ * uses -q_ij off the diagonal.  i_a == NULL (j_b == NULL) means the
+ * identity map i = e (j = e) — co-located continua.  sigma == NULL
+ * uses sigma_const.  scale_by_measure = 1 multiplies sigma by |cell_i| of continuum a
+ * (co-located field coefficient integrated over the cell, reading C9).  Several
+ * couplings may name the same pair; entries with the same (i, j) add.
+ */
+typedef struct {
+  int32_t a, b;
+  int64_t nnz;
+  const int32_t* i_a;
+  const int32_t* j_b;
+  const double* sigma;  double sigma_const;     /* sigma >= 0                             */
+  int32_t scale_by_measure;
+} mc_coupling_desc;
+
+/* Per-step report.  For MC_COUPLED there is one solve (nsolves = 1, index 0). */
+typedef struct {
+  int32_t step;                        /* time layer n reached (1-based)                  */
+  int32_t scheme;                      /* mc_scheme                                        */
+  int32_t nsolves;
+  int32_t status;                      /* mc_status of the step                            */
+  int32_t failed_solve;                /* -1, or the solve index that failed               */
+  int32_t pad;
+  int64_t iters[MC_MAX_CONTINUA];      /* CG iterations of each solve                      */
+  double relres[MC_MAX_CONTINUA];      /* final recursive ||r|| / ||b|| (0 when b = 0)     */
+  double bnorm[MC_MAX_CONTINUA];       /* ||b||_2 of each solve                            */
+  double ms_solve[MC_MAX_CONTINUA];    /* device time of each solve (globaltimer)          */
+  double ms;                           /* device time of the whole step kernel             */
+} mc_step_report;
+
+/* Create a context for n_continua (1..MC_MAX_CONTINUA) continua. */
+mc_status mc_create(mc_ctx** out, int32_t n_continua, const mc_options* opt);
+
+/* Define continuum alpha (0 <= alpha < n_continua).  May be called once per alpha. */
+mc_status mc_set_continuum(mc_ctx* ctx, int32_t alpha, const mc_continuum_desc* desc);
+
+/* Add a transfer Q_ab.  All continua must be set first (else MC_ERR_STATE). */
+mc_status mc_set_coupling(mc_ctx* ctx, const mc_coupling_desc* desc);
+
+/* Advance one time layer by the D-scheme / the coupled scheme.  Blocks until the step
+ * completed; fills *rep (may be NULL).  On MC_ERR_NOCONV / MC_ERR_BREAKDOWN the state is
+ * left at p^{n-1}. */
+mc_status mc_step_decoupled(mc_ctx* ctx, mc_step_report* rep);
+mc_status mc_step_coupled(mc_ctx* ctx, mc_step_report* rep);
+
+/* n_steps steps of `scheme`, enqueued back to back, one synchronisation at the end.
+ * reps: NULL or n_steps reports.  snapshots: NULL, or n_steps * n_continua pointers
+ * (host or device), snapshots[s * n_continua + a] receives p_a after step s.
+ * Stops advancing at the first failed step (later steps are no-ops, reports say so). */
+mc_status mc_run(mc_ctx* ctx, int32_t scheme, int32_t n_steps, mc_step_report* reps,
+                 double* const* snapshots);
+
+/* Copy the current state p_a (n_a doubles) to / from dst / src (host or device). */
+mc_status mc_get_state(mc_ctx* ctx, int32_t alpha, double* dst);
+mc_status mc_set_state(mc_ctx* ctx, int32_t alpha, const double* src);
+
+/* Sizes: n_a of continuum alpha (or the total when alpha < 0). */
+int64_t mc_size(const mc_ctx* ctx, int32_t alpha);
+
+/* CUDA-event time (ms) of the last step kernel launch, measured on mc_options.stream. */
+mc_status mc_last_kernel_ms(mc_ctx* ctx, double* ms_out);
+
+mc_status mc_destroy(mc_ctx* ctx);
+
+/* Last error message of ctx (or of the last failed mc_create when ctx == NULL). */
+const char* mc_error_string(const mc_ctx* ctx);
+
+int32_t mc_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MC_H */

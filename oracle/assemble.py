@@ -42,6 +42,18 @@ class System:
         self.F = np.asarray(F, dtype=np.float64)
         self.u0 = np.asarray(u0, dtype=np.float64)
         self.names = list(names)
+        self._flux = None
+
+    @property
+    def flux(self):
+        """Flux form of A (set by assemble(); derived from the assembled A otherwise)."""
+        if self._flux is None:
+            self._flux = flux_from_assembled(self)
+        return self._flux
+
+    @flux.setter
+    def flux(self, v):
+        self._flux = v
 
     @property
     def L(self):
@@ -210,7 +222,153 @@ def apply_dirichlet_rows(sys: System, mask, g) -> System:
 
 def assemble(scn) -> System:
     if scn["kind"] == "fine":
-        return assemble_fine(scn)
-    if scn["kind"] == "nlmc":
-        return assemble_nlmc(scn)
-    raise ValueError(scn["kind"])
+        sys_ = assemble_fine(scn)
+    elif scn["kind"] == "nlmc":
+        sys_ = assemble_nlmc(scn)
+    else:
+        raise ValueError(scn["kind"])
+    sys_.flux = flux_form(scn, sys_)
+    return sys_
+
+
+# --------------------------------------------------------------------------- flux form
+class FluxForm:
+    """The same operator A written as in Eq. app-md, unassembled:
+
+        (A p)_i = diag_i p_i + sum_{edges e = (i, j)} t_e (p_i - p_j)
+
+    over every two-point connection: TPFA faces and fracture edges (within a
+    continuum) and transfer entries sigma_ij (between continua,
+    PAPER.md:256, 260, 302), plus non-edge diagonal terms (Dirichlet half-cell faces,
+    NLMC fixed-DOF identity rows).  Assembling it gives the assembled A (pinned in
+    tests); evaluating it WITHOUT assembly avoids storing a_ii = sum T + sigma, whose
+    rounding (eps * T_f ~ 1e-7 for T_f = 1e9) swamps sigma ~ 1e2 in the fracture rows
+    (reading C15).  The oracle uses it, in long double, for iterative refinement.
+    """
+
+    def __init__(self, N, ei, ej, et, between, diag):
+        self.N = int(N)
+        self.ei = np.asarray(ei, dtype=np.int64)
+        self.ej = np.asarray(ej, dtype=np.int64)
+        self.et = np.asarray(et, dtype=np.float64)
+        self.between = np.asarray(between, dtype=bool)
+        self.diag = np.asarray(diag, dtype=np.float64)
+
+    def block_op(self, sl, mtau, scheme):
+        """Operator of one solve: coupled (whole system, all edges) or the D-scheme
+        block `sl` (A0 block: within-continuum edges, transfer edges as diagonal)."""
+        lo, hi = sl.start, sl.stop
+        if scheme == "coupled":
+            keep = np.ones(len(self.ei), dtype=bool)
+        else:
+            keep = (~self.between) & (self.ei >= lo) & (self.ei < hi)
+        d = mtau[lo:hi] + self.diag[lo:hi]
+        if scheme != "coupled":               # A0 diagonal: + sum_b Q_ab 1 (PAPER.md:462-466)
+            for end in (self.ei, self.ej):
+                m = self.between & (end >= lo) & (end < hi)
+                d = d + np.bincount(end[m] - lo, weights=self.et[m], minlength=hi - lo)
+        return BlockOp(hi - lo, self.ei[keep] - lo, self.ej[keep] - lo, self.et[keep], d)
+
+
+class BlockOp:
+    """y = d * x + sum_e t_e (x_i - x_j) on one system (flux form)."""
+
+    def __init__(self, n, ei, ej, et, d):
+        self.n, self.d = n, np.asarray(d, dtype=np.float64)
+        rows = np.concatenate([ei, ej])
+        oth = np.concatenate([ej, ei])
+        t = np.concatenate([et, et])
+        order = np.argsort(rows, kind="stable")
+        self.rows, self.oth, self.t = rows[order], oth[order], t[order]
+        self.starts = np.searchsorted(self.rows, np.arange(n))
+        self.has = np.diff(np.concatenate([self.starts, [len(self.rows)]])) > 0
+
+    def apply(self, x, dtype=np.float64):
+        x = np.asarray(x).astype(dtype)
+        y = self.d.astype(dtype) * x
+        if len(self.rows):
+            c = self.t.astype(dtype) * (x[self.rows] - x[self.oth])
+            c = np.append(c, np.zeros(1, dtype=dtype))       # sentinel: every start is a valid index
+            s = np.add.reduceat(c, self.starts)
+            y[self.has] += s[self.has]
+        return y
+
+    def tocsr(self):
+        return sp.csr_matrix(laplacian_from_edges(self.n, self.rows[self.rows < self.oth],
+                                                  self.oth[self.rows < self.oth],
+                                                  self.t[self.rows < self.oth]) + sp.diags(self.d))
+
+
+def flux_from_assembled(sys_: System) -> FluxForm:
+    """Edges t = -a_ij (i < j) and diag = a_ii - sum_j t_ij read back from an assembled A."""
+    A = sp.triu(sp.csr_matrix(sys_.A), k=1).tocoo()
+    ei, ej, et = A.row.astype(np.int64), A.col.astype(np.int64), -A.data
+    blk = lambda v: np.searchsorted(sys_.offsets, v, side="right") - 1
+    N = sys_.A.shape[0]
+    rs = np.bincount(ei, weights=et, minlength=N) + np.bincount(ej, weights=et, minlength=N)
+    return FluxForm(N, ei, ej, et, blk(ei) != blk(ej), sys_.A.diagonal() - rs)
+
+
+def flux_form(scn, sys_: System) -> FluxForm:
+    off = sys_.offsets
+    EI, EJ, ET, BT = [], [], [], []
+    diag = np.zeros(int(off[-1]))
+    if scn["kind"] == "fine":
+        n, h = scn["n"], scn["h"]
+        for a, cont in enumerate(scn["continua"]):
+            if cont["kind"] == "grid":
+                fi, fj = grid_faces(n, n)
+                EI.append(off[a] + fi)
+                EJ.append(off[a] + fj)
+                ET.append(face_transmissibility(cont["k"], fi, fj))
+                BT.append(np.zeros(len(fi), dtype=bool))
+                if cont["dirichlet"] is not None:
+                    kk = np.full(n * n, float(cont["k"])) if np.ndim(cont["k"]) == 0 else cont["k"]
+                    ix = np.arange(n * n) % n
+                    for col, g in ((0, cont["dirichlet"][0]), (n - 1, cont["dirichlet"][1])):
+                        if g is not None:
+                            cells = np.nonzero(ix == col)[0]
+                            diag[off[a] + cells] += kk[cells] * h / (h / 2.0)     # C3
+            else:
+                e = np.asarray(scn["fracture"]["edges"], dtype=np.int64).reshape(-1, 2)
+                EI.append(off[a] + e[:, 0])
+                EJ.append(off[a] + e[:, 1])
+                ET.append(np.full(len(e), float(cont["k"]) / h))                 # C7
+                BT.append(np.zeros(len(e), dtype=bool))
+        for cp in scn["couplings"]:
+            a, b = cp["a"], cp["b"]
+            if cp["type"] == "embedded":
+                cells = scn["fracture"]["cells"]
+                EI.append(off[a] + cells)
+                EJ.append(off[b] + np.arange(len(cells)))
+                ET.append(np.asarray(cp["sigma"], dtype=np.float64))              # C6
+            else:
+                m = n * n
+                EI.append(off[a] + np.arange(m))
+                EJ.append(off[b] + np.arange(m))
+                ET.append(np.full(m, float(cp["sigma"]) * h * h))                # C9
+            BT.append(np.ones(len(EI[-1]), dtype=bool))
+        return FluxForm(off[-1], np.concatenate(EI), np.concatenate(EJ), np.concatenate(ET),
+                        np.concatenate(BT), diag)
+    # NLMC with fixed-DOF identity rows (C12): edges touching a fixed DOF leave the
+    # operator; their t stays on the free endpoint's diagonal (its F got t g).
+    Nb = scn["nc"] ** 2
+    mask = np.concatenate([scn["dirichlet"][a][0] for a in range(2)])
+    for a, (i, j, t) in enumerate(scn["within"]):
+        EI.append(a * Nb + i)
+        EJ.append(a * Nb + j)
+        ET.append(t)
+        BT.append(np.zeros(len(i), dtype=bool))
+    bi, bj, bt = scn["between"]
+    EI.append(bi)
+    EJ.append(Nb + bj)
+    ET.append(bt)
+    BT.append(np.ones(len(bi), dtype=bool))
+    ei, ej, et, bw = (np.concatenate(v) for v in (EI, EJ, ET, BT))
+    fi, fj = mask[ei], mask[ej]
+    for end, other in ((ei, fj), (ej, fi)):
+        sel = other & ~mask[end]
+        diag += np.bincount(end[sel], weights=et[sel], minlength=2 * Nb)
+    diag[mask] = 1.0
+    keep = ~fi & ~fj
+    return FluxForm(2 * Nb, ei[keep], ej[keep], et[keep], bw[keep], diag)

@@ -34,33 +34,69 @@ def split_D(sys: System):
 
 
 class _Solver:
-    """x = K^{-1} b via SuperLU ('splu') or Jacobi-PCG ('cg', warm start x0)."""
+    """x = K^{-1} b for one solve.
 
-    def __init__(self, K, method="splu", rtol=1e-13):
-        self.K = sp.csc_matrix(K)
+    'splu': SuperLU factorisation of the assembled K, then iterative refinement
+            x += K^{-1}(b - K x) with the residual evaluated in long double on the
+            unassembled flux form (FluxForm), until the correction
+            is below 1e-16 ||x||.  The result is the solution of the exact operator,
+            not of its fp64-rounded assembly (reading C15).
+    'cg':   plain Jacobi-PCG (oracle.cg) on the flux-form operator in fp64.
+    """
+
+    def __init__(self, op, method="splu", rtol=1e-13, refine=True):
+        self.op = op
         self.method = method
         self.rtol = rtol
+        self.refine = refine
         self.iters = []
+        self.refinements = []
+        self.K = sp.csc_matrix(op.tocsr())
         if method == "splu":
             self.lu = spla.splu(self.K)
         elif method != "cg":
             raise ValueError(method)
 
     def solve(self, b, x0):
-        if self.method == "splu":
-            return self.lu.solve(b)
-        x, it = _cg.jacobi_pcg(sp.csr_matrix(self.K), b, x0, rtol=self.rtol, maxit=10 * len(b) + 10)
-        self.iters.append(it)
+        if self.method == "cg":
+            x, it = _cg.jacobi_pcg(_FluxMatvec(self.op, self.K.diagonal()), b, x0, rtol=self.rtol,
+                                   maxit=10 * len(b) + 10)
+            self.iters.append(it)
+            return x
+        x = self.lu.solve(b)
+        k = 0
+        if self.refine and np.any(x):
+            bl = np.asarray(b, dtype=np.longdouble)
+            for k in range(1, 9):
+                r = np.asarray(bl - self.op.apply(x, np.longdouble), dtype=np.float64)
+                dx = self.lu.solve(r)
+                x = x + dx
+                if np.linalg.norm(dx) <= 1e-16 * np.linalg.norm(x):
+                    break
+        self.refinements.append(k)
         return x
+
+
+class _FluxMatvec:
+    """K p via the flux form (for the CG oracle); .diagonal() for Jacobi."""
+
+    def __init__(self, op, diag):
+        self.op, self._d = op, diag
+
+    def __matmul__(self, x):
+        return self.op.apply(x)
+
+    def diagonal(self):
+        return self._d
 
 
 class Coupled:
     """Coupled backward-Euler stepper on the whole system (Eq. ct-mc)."""
 
-    def __init__(self, sys: System, tau: float, method="splu"):
+    def __init__(self, sys: System, tau: float, method="splu", refine=True):
         self.sys, self.tau = sys, float(tau)
-        K = sp.diags(sys.M / self.tau) + sys.A
-        self.solver = _Solver(K, method)
+        op = sys.flux.block_op(slice(0, int(sys.offsets[-1])), sys.M / self.tau, "coupled")
+        self.solver = _Solver(op, method, refine=refine)
 
     def step(self, u):
         b = self.sys.M / self.tau * u + self.sys.F
@@ -70,14 +106,13 @@ class Coupled:
 class DScheme:
     """Decoupled D-scheme stepper (Eq. si-mc, D-split): L independent solves per step."""
 
-    def __init__(self, sys: System, tau: float, method="splu"):
+    def __init__(self, sys: System, tau: float, method="splu", refine=True):
         self.sys, self.tau = sys, float(tau)
         self.A0, self.A1 = split_D(sys)
-        K0 = sp.csr_matrix(sp.diags(sys.M / self.tau) + self.A0)
         self.solvers = []
         for a in range(sys.L):
-            s = sys.block(a)
-            self.solvers.append(_Solver(K0[s, s], method))
+            op = sys.flux.block_op(sys.block(a), sys.M / self.tau, "D")
+            self.solvers.append(_Solver(op, method, refine=refine))
 
     def rhs(self, u):
         """b = M/tau p^{n-1} + F - A1 p^{n-1}: every coupling term from layer n-1."""
@@ -92,17 +127,17 @@ class DScheme:
         return out
 
 
-def make_stepper(sys: System, scheme: str, tau: float, method="splu"):
+def make_stepper(sys: System, scheme: str, tau: float, method="splu", refine=True):
     if scheme == "coupled":
-        return Coupled(sys, tau, method)
+        return Coupled(sys, tau, method, refine)
     if scheme in ("D", "decoupled", "d"):
-        return DScheme(sys, tau, method)
+        return DScheme(sys, tau, method, refine)
     raise ValueError(scheme)
 
 
-def run(sys: System, scheme: str, tau: float, n_steps: int, method="splu", u0=None):
+def run(sys: System, scheme: str, tau: float, n_steps: int, method="splu", u0=None, refine=True):
     """Trajectory [p^1, ..., p^n_steps] (full concatenated vectors)."""
-    st = make_stepper(sys, scheme, tau, method)
+    st = make_stepper(sys, scheme, tau, method, refine)
     u = sys.u0.copy() if u0 is None else np.asarray(u0, dtype=np.float64).copy()
     out = []
     for _ in range(n_steps):

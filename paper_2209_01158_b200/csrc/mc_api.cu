@@ -1,0 +1,960 @@
+// mc_api.cu — host side of libmc: the C ABI of include/mc.h.
+//
+// Setup (mc_set_continuum / mc_set_coupling, finalised lazily before the first step)
+// derives the operator arrays of Eq. app-mc from the physical
+// inputs in native C++ and uploads them once; every step is one cooperative launch
+// of the sm_100a step kernel (mc_kernels.cu).  Readings C1-C15 of DESIGN.md §3.
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <numeric>
+#include <string>
+#include <vector>
+
+#include "mc_internal.h"
+
+using namespace mc;
+
+namespace {
+
+constexpr int64_t kLargeRows = int64_t(2) << 20;   // "bandwidth-bound" solve
+
+struct HostCont {
+  bool set = false;
+  int32_t kind = 0;
+  int64_t n = 0;
+  int32_t nx = 0, ny = 0;
+  double h = 0.0;
+  std::vector<double> mtau, dbase, F, u0, tsum, measure;
+  std::vector<double> Tx, Ty;                  // grid
+  std::vector<int32_t> rowptr, col;            // graph, local columns
+  std::vector<double> val;                     // graph per-entry T (empty -> uniform)
+  double Tconst = 0.0;
+  std::vector<uint8_t> fixed;                  // graph Dirichlet DOFs
+  std::vector<double> gfix;
+};
+
+struct HostCoupling {
+  int32_t a = 0, b = 0;
+  std::vector<int32_t> i, j;
+  std::vector<double> s;
+};
+
+struct Plan {
+  int nphases = 0, ngroups = 0;
+  Group grp[MC_MAX_CONTINUA];
+  std::vector<Item> items;
+  bool valid = false;
+};
+
+}  // namespace
+
+struct mc_ctx {
+  mc_options opt{};
+  int32_t L = 0;
+  std::string err;
+  HostCont hc[MC_MAX_CONTINUA];
+  std::vector<HostCoupling> cpl;
+  bool finalized = false;
+  cudaStream_t stream = nullptr;
+  int sms = 0, occ = 0, total_ctas = 0;
+  // device
+  int64_t off[MC_MAX_CONTINUA + 1] = {0};
+  int64_t N = 0;
+  double* u[2] = {nullptr, nullptr};
+  double* r[2] = {nullptr, nullptr};
+  double* p[2] = {nullptr, nullptr};
+  double* q[2] = {nullptr, nullptr};
+  double *dinv = nullptr, *dsD = nullptr, *dsC = nullptr, *mtau = nullptr, *F = nullptr;
+  int32_t *cptr = nullptr, *cidx = nullptr;
+  double* cval = nullptr;
+  double* Tx[MC_MAX_CONTINUA] = {nullptr};
+  double* Ty[MC_MAX_CONTINUA] = {nullptr};
+  int32_t* rowptr[MC_MAX_CONTINUA] = {nullptr};
+  int32_t* col[MC_MAX_CONTINUA] = {nullptr};
+  double* val[MC_MAX_CONTINUA] = {nullptr};
+  double* partials = nullptr;
+  SyncBlock* sync = nullptr;
+  GroupOut* gout = nullptr;
+  int32_t* cur = nullptr;
+  int32_t* fail = nullptr;
+  mc_step_report* rep = nullptr;
+  Item* items = nullptr;
+  size_t items_cap = 0;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  int32_t cur_host = 0;
+  int32_t step_no = 0;
+  int64_t last_iters[MC_MAX_CONTINUA] = {0};
+  Plan plan[2];                                 // by scheme
+  int uploaded_plan = -1;                       // scheme whose items are on device
+  std::vector<void*> allocs;
+};
+
+static std::string g_create_err;
+
+namespace {
+
+mc_status fail(mc_ctx* c, mc_status st, const char* fmt, ...) {
+  char buf[1024];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  if (c) c->err = buf;
+  else g_create_err = buf;
+  return st;
+}
+
+#define CUDA_TRY(c, call)                                                                     \
+  do {                                                                                        \
+    cudaError_t e_ = (call);                                                                  \
+    if (e_ != cudaSuccess)                                                                    \
+      return fail((c), e_ == cudaErrorMemoryAllocation ? MC_ERR_NOMEM : MC_ERR_CUDA,          \
+                  "%s: %s (%s:%d)", #call, cudaGetErrorString(e_), __FILE__, __LINE__);       \
+  } while (0)
+
+template <class T>
+mc_status dev_alloc(mc_ctx* c, T** p, size_t count) {
+  void* v = nullptr;
+  CUDA_TRY(c, cudaMalloc(&v, std::max<size_t>(count, 1) * sizeof(T)));
+  c->allocs.push_back(v);
+  *p = static_cast<T*>(v);
+  return MC_OK;
+}
+
+// copy `count` elements from a host or device pointer into a host vector
+template <class T>
+mc_status fetch(mc_ctx* c, std::vector<T>& dst, const T* src, int64_t count) {
+  dst.resize((size_t)count);
+  if (count == 0) return MC_OK;
+  CUDA_TRY(c, cudaMemcpy(dst.data(), src, (size_t)count * sizeof(T), cudaMemcpyDefault));
+  return MC_OK;
+}
+
+template <class T>
+mc_status upload(mc_ctx* c, T** dst, const std::vector<T>& src) {
+  mc_status st = dev_alloc(c, dst, src.size());
+  if (st != MC_OK) return st;
+  if (!src.empty())
+    CUDA_TRY(c, cudaMemcpyAsync(*dst, src.data(), src.size() * sizeof(T), cudaMemcpyHostToDevice,
+                                c->stream));
+  return MC_OK;
+}
+
+bool finite_nonneg(double v) { return std::isfinite(v) && v >= 0.0; }
+
+mc_status field(mc_ctx* c, std::vector<double>& out, const double* ptr, double cst, int64_t n,
+                const char* name, bool positive) {
+  if (ptr) {
+    mc_status st = fetch(c, out, ptr, n);
+    if (st != MC_OK) return st;
+  } else {
+    out.assign((size_t)n, cst);
+  }
+  for (int64_t i = 0; i < n; ++i) {
+    const double v = out[(size_t)i];
+    if (!finite_nonneg(v) || (positive && !(v > 0.0)))
+      return fail(c, MC_ERR_ARG, "%s[%lld] = %g is not %s", name, (long long)i, v,
+                  positive ? "finite and > 0" : "finite and >= 0");
+  }
+  return MC_OK;
+}
+
+double harmonic(double a, double b) { return (a + b) > 0.0 ? 2.0 * a * b / (a + b) : 0.0; }
+
+}  // namespace
+
+// ====================================================================== create / destroy
+extern "C" int32_t mc_abi_version(void) { return MC_ABI_VERSION; }
+
+extern "C" const char* mc_error_string(const mc_ctx* ctx) {
+  return ctx ? ctx->err.c_str() : g_create_err.c_str();
+}
+
+extern "C" mc_status mc_create(mc_ctx** out, int32_t n_continua, const mc_options* opt) {
+  if (!out) return fail(nullptr, MC_ERR_ARG, "out is NULL");
+  *out = nullptr;
+  if (n_continua < 1 || n_continua > MC_MAX_CONTINUA)
+    return fail(nullptr, MC_ERR_ARG, "n_continua = %d not in [1, %d]", n_continua, MC_MAX_CONTINUA);
+  if (!opt) return fail(nullptr, MC_ERR_ARG, "opt is NULL");
+  if (!(std::isfinite(opt->tau) && opt->tau > 0.0))
+    return fail(nullptr, MC_ERR_ARG, "tau = %g must be finite and > 0", opt->tau);
+  if (!std::isfinite(opt->rtol) || opt->rtol >= 1.0)
+    return fail(nullptr, MC_ERR_ARG, "rtol = %g must be < 1", opt->rtol);
+  int ndev = 0;
+  cudaError_t e = cudaGetDeviceCount(&ndev);
+  if (e != cudaSuccess || ndev == 0)
+    return fail(nullptr, MC_ERR_CUDA, "no CUDA device: %s", cudaGetErrorString(e));
+  if (opt->device < 0 || opt->device >= ndev)
+    return fail(nullptr, MC_ERR_ARG, "device %d not in [0, %d)", opt->device, ndev);
+  mc_ctx* c = new mc_ctx();
+  c->opt = *opt;
+  if (!(c->opt.rtol > 0.0)) c->opt.rtol = 1e-12;
+  c->L = n_continua;
+  c->stream = static_cast<cudaStream_t>(opt->stream);
+  e = cudaSetDevice(opt->device);
+  if (e == cudaSuccess) e = cudaDeviceGetAttribute(&c->sms, cudaDevAttrMultiProcessorCount, opt->device);
+  if (e == cudaSuccess) e = step_kernel_occupancy(&c->occ);
+  if (e == cudaSuccess) e = cudaEventCreate(&c->ev0);
+  if (e == cudaSuccess) e = cudaEventCreate(&c->ev1);
+  if (e != cudaSuccess) {
+    fail(nullptr, MC_ERR_CUDA, "device setup: %s", cudaGetErrorString(e));
+    delete c;
+    return MC_ERR_CUDA;
+  }
+  int coop = 0;
+  cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, opt->device);
+  if (!coop || c->occ < 1) {
+    fail(nullptr, MC_ERR_CUDA, "device lacks cooperative launch (occupancy %d)", c->occ);
+    delete c;
+    return MC_ERR_CUDA;
+  }
+  const int maxc = c->sms * c->occ;
+  c->total_ctas = (opt->ctas > 0) ? std::min(opt->ctas, maxc) : maxc;
+  *out = c;
+  return MC_OK;
+}
+
+extern "C" mc_status mc_destroy(mc_ctx* c) {
+  if (!c) return MC_OK;
+  cudaStreamSynchronize(c->stream);
+  for (void* v : c->allocs) cudaFree(v);
+  if (c->ev0) cudaEventDestroy(c->ev0);
+  if (c->ev1) cudaEventDestroy(c->ev1);
+  delete c;
+  return MC_OK;
+}
+
+extern "C" int64_t mc_size(const mc_ctx* c, int32_t alpha) {
+  if (!c) return -1;
+  if (alpha < 0) {
+    int64_t s = 0;
+    for (int a = 0; a < c->L; ++a) s += c->hc[a].n;
+    return s;
+  }
+  if (alpha >= c->L) return -1;
+  return c->hc[alpha].n;
+}
+
+// ====================================================================== continua
+static mc_status set_grid(mc_ctx* c, HostCont& H, const mc_continuum_desc* d) {
+  const int64_t n = d->n;
+  if (d->nx < 1 || d->ny < 1 || (int64_t)d->nx * d->ny != n)
+    return fail(c, MC_ERR_ARG, "grid nx*ny = %d*%d != n = %lld", d->nx, d->ny, (long long)n);
+  if (!(std::isfinite(d->h) && d->h > 0.0)) return fail(c, MC_ERR_ARG, "grid h = %g must be > 0", d->h);
+  if ((d->bc_left != 0 && d->bc_left != 1) || (d->bc_right != 0 && d->bc_right != 1))
+    return fail(c, MC_ERR_ARG, "bc_left/bc_right must be 0 (no-flow) or 1 (Dirichlet)");
+  if ((d->bc_left && !std::isfinite(d->g_left)) || (d->bc_right && !std::isfinite(d->g_right)))
+    return fail(c, MC_ERR_ARG, "Dirichlet value not finite");
+  const int nx = d->nx, ny = d->ny;
+  const double h = d->h, tau = c->opt.tau, area = h * h;   // |cell| = h^2 (reading C1)
+  std::vector<double> k, cc, f;
+  mc_status st;
+  if ((st = field(c, k, d->k, d->k_const, n, "k", false)) != MC_OK) return st;
+  if ((st = field(c, cc, d->c, d->c_const, n, "c", false)) != MC_OK) return st;
+  if (d->f) {
+    if ((st = fetch(c, f, d->f, n)) != MC_OK) return st;
+    for (double v : f)
+      if (!std::isfinite(v)) return fail(c, MC_ERR_ARG, "source f not finite");
+  }
+  H.kind = KIND_GRID;
+  H.n = n;
+  H.nx = nx;
+  H.ny = ny;
+  H.h = h;
+  H.Tx.assign((size_t)n, 0.0);
+  H.Ty.assign((size_t)n, 0.0);
+  H.tsum.assign((size_t)n, 0.0);
+  H.mtau.resize((size_t)n);
+  H.dbase.resize((size_t)n);
+  H.F.assign((size_t)n, 0.0);
+  H.measure.assign((size_t)n, area);
+  const bool kc = (d->k == nullptr);
+  // T = k |E|/d, |E| = d = h; harmonic mean for a k field (reading C2)
+  for (int iy = 0; iy < ny; ++iy)
+    for (int ix = 0; ix < nx; ++ix) {
+      const int64_t i = (int64_t)iy * nx + ix;
+      if (ix + 1 < nx) H.Tx[(size_t)i] = kc ? d->k_const : harmonic(k[(size_t)i], k[(size_t)i + 1]);
+      if (iy + 1 < ny) H.Ty[(size_t)i] = kc ? d->k_const : harmonic(k[(size_t)i], k[(size_t)(i + nx)]);
+    }
+  for (int iy = 0; iy < ny; ++iy)
+    for (int ix = 0; ix < nx; ++ix) {
+      const size_t i = (size_t)iy * nx + ix;
+      double ts = H.Tx[i] + H.Ty[i];
+      if (ix > 0) ts += H.Tx[i - 1];
+      if (iy > 0) ts += H.Ty[i - nx];
+      H.tsum[i] = ts;
+      const double m = cc[i] * area;                       // m = c |cell|
+      H.mtau[i] = m / tau;
+      double db = 0.0, Fi = f.empty() ? 0.0 : f[i] * area;  // F = f |cell|
+      // Dirichlet face, half-cell distance: T_b = k h / (h/2) (reading C3)
+      if (ix == 0 && d->bc_left) {
+        const double tb = k[i] * h / (h / 2.0);
+        db += tb;
+        Fi += tb * d->g_left;
+      }
+      if (ix == nx - 1 && d->bc_right) {
+        const double tb = k[i] * h / (h / 2.0);
+        db += tb;
+        Fi += tb * d->g_right;
+      }
+      H.dbase[i] = H.mtau[i] + db;
+      H.F[i] = Fi;
+    }
+  return MC_OK;
+}
+
+static mc_status set_graph(mc_ctx* c, HostCont& H, const mc_continuum_desc* d) {
+  const int64_t n = d->n, E = d->n_edges;
+  if (n > INT32_MAX - 1) return fail(c, MC_ERR_ARG, "graph n too large for int32 indices");
+  if (E < 0) return fail(c, MC_ERR_ARG, "n_edges < 0");
+  if (E > 0 && (!d->edge_i || !d->edge_j)) return fail(c, MC_ERR_ARG, "edge_i / edge_j NULL");
+  if (E > 0 && !d->edge_t && !(std::isfinite(d->edge_geom) && d->edge_geom >= 0.0))
+    return fail(c, MC_ERR_ARG, "edge_geom = %g must be finite and >= 0", d->edge_geom);
+  const double tau = c->opt.tau;
+  std::vector<double> k, cc, f, meas, et, dir;
+  std::vector<int32_t> ei, ej;
+  mc_status st;
+  if ((st = field(c, k, d->k, d->k_const, n, "k", false)) != MC_OK) return st;
+  if ((st = field(c, cc, d->c, d->c_const, n, "c", false)) != MC_OK) return st;
+  if ((st = field(c, meas, d->measure, d->measure_const, n, "measure", true)) != MC_OK) return st;
+  if (d->f) {
+    if ((st = fetch(c, f, d->f, n)) != MC_OK) return st;
+    for (double v : f)
+      if (!std::isfinite(v)) return fail(c, MC_ERR_ARG, "source f not finite");
+  }
+  if ((st = fetch(c, ei, d->edge_i, E)) != MC_OK) return st;
+  if ((st = fetch(c, ej, d->edge_j, E)) != MC_OK) return st;
+  if (d->edge_t) {
+    if ((st = fetch(c, et, d->edge_t, E)) != MC_OK) return st;
+  }
+  if (d->dirichlet) {
+    if ((st = fetch(c, dir, d->dirichlet, n)) != MC_OK) return st;
+    for (double v : dir)
+      if (std::isinf(v)) return fail(c, MC_ERR_ARG, "dirichlet value infinite");
+  }
+  // edges: range, self-loops, duplicates
+  std::vector<int64_t> key((size_t)E);
+  for (int64_t e = 0; e < E; ++e) {
+    const int32_t a = ei[(size_t)e], b = ej[(size_t)e];
+    if (a < 0 || b < 0 || a >= n || b >= n || a == b)
+      return fail(c, MC_ERR_ARG, "edge %lld = (%d, %d) out of range or self-loop", (long long)e, a, b);
+    key[(size_t)e] = (int64_t)std::min(a, b) * n + std::max(a, b);
+    if (d->edge_t && !finite_nonneg(et[(size_t)e]))
+      return fail(c, MC_ERR_ARG, "edge_t[%lld] = %g must be finite and >= 0", (long long)e, et[(size_t)e]);
+  }
+  {
+    std::vector<int64_t> ks(key);
+    std::sort(ks.begin(), ks.end());
+    if (std::adjacent_find(ks.begin(), ks.end()) != ks.end())
+      return fail(c, MC_ERR_ARG, "duplicate edge in graph continuum");
+  }
+  H.kind = KIND_GRAPH;
+  H.n = n;
+  H.measure = meas;
+  H.mtau.resize((size_t)n);
+  H.dbase.resize((size_t)n);
+  H.F.assign((size_t)n, 0.0);
+  H.tsum.assign((size_t)n, 0.0);
+  H.fixed.assign((size_t)n, 0);
+  H.gfix.assign((size_t)n, 0.0);
+  for (int64_t i = 0; i < n; ++i) {
+    const size_t s = (size_t)i;
+    H.mtau[s] = cc[s] * meas[s] / tau;                       // m = c |cell|
+    H.dbase[s] = H.mtau[s];
+    H.F[s] = f.empty() ? 0.0 : f[s] * meas[s];
+    if (!dir.empty() && !std::isnan(dir[s])) {                // fixed DOF: identity row (C12)
+      H.fixed[s] = 1;
+      H.gfix[s] = dir[s];
+      H.mtau[s] = 0.0;
+      H.dbase[s] = 1.0;
+      H.F[s] = dir[s];
+    }
+  }
+  // edge transmissibilities T_e = k |E|/d, harmonic k for a field
+  std::vector<double> T((size_t)E);
+  const bool kc = (d->k == nullptr);
+  for (int64_t e = 0; e < E; ++e) {
+    const int32_t a = ei[(size_t)e], b = ej[(size_t)e];
+    T[(size_t)e] = d->edge_t ? et[(size_t)e]
+                             : (kc ? d->k_const : harmonic(k[(size_t)a], k[(size_t)b])) * d->edge_geom;
+  }
+  // CSR of free-free edges; edges to fixed DOFs eliminated into diagonal and F (C12)
+  std::vector<int32_t> cnt((size_t)n + 1, 0);
+  for (int64_t e = 0; e < E; ++e) {
+    const int32_t a = ei[(size_t)e], b = ej[(size_t)e];
+    const bool fa = H.fixed[(size_t)a], fb = H.fixed[(size_t)b];
+    if (!fa && !fb) {
+      cnt[(size_t)a + 1]++;
+      cnt[(size_t)b + 1]++;
+    } else if (!fa && fb) {
+      H.dbase[(size_t)a] += T[(size_t)e];
+      H.F[(size_t)a] += T[(size_t)e] * H.gfix[(size_t)b];
+    } else if (fa && !fb) {
+      H.dbase[(size_t)b] += T[(size_t)e];
+      H.F[(size_t)b] += T[(size_t)e] * H.gfix[(size_t)a];
+    }
+  }
+  for (size_t i = 0; i < (size_t)n; ++i) cnt[i + 1] += cnt[i];
+  if (cnt[(size_t)n] > INT32_MAX / 2) return fail(c, MC_ERR_ARG, "graph too large for int32 CSR");
+  H.rowptr = cnt;
+  H.col.assign((size_t)cnt[(size_t)n], 0);
+  std::vector<double> vals((size_t)cnt[(size_t)n]);
+  std::vector<int32_t> pos(cnt.begin(), cnt.end() - 1);
+  bool uniform = true;
+  double t0 = E > 0 ? T[0] : 0.0;
+  for (int64_t e = 0; e < E; ++e) {
+    const int32_t a = ei[(size_t)e], b = ej[(size_t)e];
+    if (H.fixed[(size_t)a] || H.fixed[(size_t)b]) continue;
+    const double t = T[(size_t)e];
+    if (t != t0) uniform = false;
+    H.col[(size_t)pos[(size_t)a]] = b;
+    vals[(size_t)pos[(size_t)a]++] = t;
+    H.col[(size_t)pos[(size_t)b]] = a;
+    vals[(size_t)pos[(size_t)b]++] = t;
+    H.tsum[(size_t)a] += t;
+    H.tsum[(size_t)b] += t;
+  }
+  // sort each row by column (deterministic, cache-friendlier gathers)
+  for (int64_t i = 0; i < n; ++i) {
+    const int32_t b0 = H.rowptr[(size_t)i], b1 = H.rowptr[(size_t)i + 1];
+    std::vector<std::pair<int32_t, double>> row;
+    row.reserve((size_t)(b1 - b0));
+    for (int32_t e = b0; e < b1; ++e) row.emplace_back(H.col[(size_t)e], vals[(size_t)e]);
+    std::sort(row.begin(), row.end());
+    for (int32_t e = b0; e < b1; ++e) {
+      H.col[(size_t)e] = row[(size_t)(e - b0)].first;
+      vals[(size_t)e] = row[(size_t)(e - b0)].second;
+    }
+  }
+  if (uniform) {
+    H.val.clear();
+    H.Tconst = t0;
+  } else {
+    H.val = std::move(vals);
+    H.Tconst = 0.0;
+  }
+  return MC_OK;
+}
+
+extern "C" mc_status mc_set_continuum(mc_ctx* c, int32_t alpha, const mc_continuum_desc* d) {
+  if (!c || !d) return fail(c, MC_ERR_ARG, "NULL argument");
+  if (alpha < 0 || alpha >= c->L) return fail(c, MC_ERR_ARG, "alpha = %d not in [0, %d)", alpha, c->L);
+  if (c->finalized) return fail(c, MC_ERR_STATE, "continuum %d set after the first step", alpha);
+  if (c->hc[alpha].set) return fail(c, MC_ERR_STATE, "continuum %d already set", alpha);
+  if (d->n < 1) return fail(c, MC_ERR_ARG, "continuum %d: n = %lld < 1", alpha, (long long)d->n);
+  if (d->n > (int64_t)INT32_MAX / 2) return fail(c, MC_ERR_ARG, "continuum %d too large", alpha);
+  HostCont H;
+  mc_status st;
+  if (d->kind == MC_GRID2D) st = set_grid(c, H, d);
+  else if (d->kind == MC_GRAPH) st = set_graph(c, H, d);
+  else return fail(c, MC_ERR_ARG, "continuum %d: unknown kind %d", alpha, (int)d->kind);
+  if (st != MC_OK) {
+    c->err = "continuum " + std::to_string(alpha) + ": " + c->err;
+    return st;
+  }
+  if (d->u0) {
+    if ((st = fetch(c, H.u0, d->u0, d->n)) != MC_OK) return st;
+    for (double v : H.u0)
+      if (!std::isfinite(v)) return fail(c, MC_ERR_ARG, "continuum %d: u0 not finite", alpha);
+  } else {
+    H.u0.assign((size_t)d->n, 0.0);
+  }
+  if (H.kind == KIND_GRAPH)
+    for (size_t i = 0; i < H.fixed.size(); ++i)
+      if (H.fixed[i]) H.u0[i] = H.gfix[i];                     // fixed DOF starts at g (C12)
+  H.set = true;
+  c->hc[alpha] = std::move(H);
+  return MC_OK;
+}
+
+// ====================================================================== couplings
+extern "C" mc_status mc_set_coupling(mc_ctx* c, const mc_coupling_desc* d) {
+  if (!c || !d) return fail(c, MC_ERR_ARG, "NULL argument");
+  if (c->finalized) return fail(c, MC_ERR_STATE, "coupling set after the first step");
+  if (d->a < 0 || d->b < 0 || d->a >= c->L || d->b >= c->L || d->a == d->b)
+    return fail(c, MC_ERR_ARG, "coupling pair (%d, %d) invalid", d->a, d->b);
+  for (int a = 0; a < c->L; ++a)
+    if (!c->hc[a].set) return fail(c, MC_ERR_STATE, "coupling before continuum %d was set", a);
+  if (d->nnz < 0) return fail(c, MC_ERR_ARG, "coupling nnz < 0");
+  const HostCont& A = c->hc[d->a];
+  const HostCont& B = c->hc[d->b];
+  HostCoupling hcp;
+  hcp.a = d->a;
+  hcp.b = d->b;
+  mc_status st;
+  const int64_t m = d->nnz;
+  if (d->i_a) {
+    if ((st = fetch(c, hcp.i, d->i_a, m)) != MC_OK) return st;
+  } else {
+    if (m > A.n) return fail(c, MC_ERR_ARG, "identity coupling nnz %lld > n_a", (long long)m);
+    hcp.i.resize((size_t)m);
+    std::iota(hcp.i.begin(), hcp.i.end(), 0);
+  }
+  if (d->j_b) {
+    if ((st = fetch(c, hcp.j, d->j_b, m)) != MC_OK) return st;
+  } else {
+    if (m > B.n) return fail(c, MC_ERR_ARG, "identity coupling nnz %lld > n_b", (long long)m);
+    hcp.j.resize((size_t)m);
+    std::iota(hcp.j.begin(), hcp.j.end(), 0);
+  }
+  if ((st = field(c, hcp.s, d->sigma, d->sigma_const, m, "sigma", false)) != MC_OK) return st;
+  for (int64_t e = 0; e < m; ++e) {
+    const int32_t i = hcp.i[(size_t)e], j = hcp.j[(size_t)e];
+    if (i < 0 || i >= A.n || j < 0 || j >= B.n)
+      return fail(c, MC_ERR_ARG, "coupling entry %lld = (%d, %d) out of range", (long long)e, i, j);
+    if (d->scale_by_measure) hcp.s[(size_t)e] *= A.measure[(size_t)i];   // sigma |cell| (C9)
+  }
+  c->cpl.push_back(std::move(hcp));
+  return MC_OK;
+}
+
+// ====================================================================== finalize
+static mc_status finalize(mc_ctx* c) {
+  if (c->finalized) return MC_OK;
+  for (int a = 0; a < c->L; ++a)
+    if (!c->hc[a].set) return fail(c, MC_ERR_STATE, "continuum %d not set", a);
+  // padded offsets (256 B) so no cache line is shared by two continua
+  int64_t o = 0;
+  for (int a = 0; a < c->L; ++a) {
+    c->off[a] = o;
+    o += (c->hc[a].n + kPadDofs - 1) / kPadDofs * kPadDofs;
+  }
+  c->off[c->L] = o;
+  c->N = o;
+  const int64_t N = c->N;
+  if (N + 1 > INT32_MAX) return fail(c, MC_ERR_ARG, "total size exceeds int32 indexing");
+  std::vector<double> mtau((size_t)N, 0.0), dbase((size_t)N, 0.0), F((size_t)N, 0.0),
+      u0((size_t)N, 0.0), tsum((size_t)N, 0.0), sig((size_t)N, 0.0);
+  for (int a = 0; a < c->L; ++a) {
+    HostCont& H = c->hc[a];
+    const size_t off = (size_t)c->off[a];
+    std::copy(H.mtau.begin(), H.mtau.end(), mtau.begin() + off);
+    std::copy(H.dbase.begin(), H.dbase.end(), dbase.begin() + off);
+    std::copy(H.F.begin(), H.F.end(), F.begin() + off);
+    std::copy(H.u0.begin(), H.u0.end(), u0.begin() + off);
+    std::copy(H.tsum.begin(), H.tsum.end(), tsum.begin() + off);
+  }
+  // couplings -> global CSR (both directions); fixed endpoints eliminated (C12)
+  std::vector<int32_t> cnt((size_t)N + 1, 0);
+  auto fixed = [&](int a, int32_t i) {
+    return c->hc[a].kind == KIND_GRAPH && c->hc[a].fixed[(size_t)i];
+  };
+  for (const HostCoupling& h : c->cpl)
+    for (size_t e = 0; e < h.i.size(); ++e) {
+      const bool fa = fixed(h.a, h.i[e]), fb = fixed(h.b, h.j[e]);
+      if (!fa && !fb) {
+        cnt[(size_t)(c->off[h.a] + h.i[e]) + 1]++;
+        cnt[(size_t)(c->off[h.b] + h.j[e]) + 1]++;
+      }
+    }
+  for (size_t i = 0; i < (size_t)N; ++i) cnt[i + 1] += cnt[i];
+  std::vector<int32_t> cidx((size_t)cnt[(size_t)N]);
+  std::vector<double> cval((size_t)cnt[(size_t)N]);
+  std::vector<int32_t> pos(cnt.begin(), cnt.end() - 1);
+  for (const HostCoupling& h : c->cpl)
+    for (size_t e = 0; e < h.i.size(); ++e) {
+      const int64_t gi = c->off[h.a] + h.i[e], gj = c->off[h.b] + h.j[e];
+      const double s = h.s[e];
+      const bool fa = fixed(h.a, h.i[e]), fb = fixed(h.b, h.j[e]);
+      if (!fa && !fb) {
+        cidx[(size_t)pos[(size_t)gi]] = (int32_t)gj;
+        cval[(size_t)pos[(size_t)gi]++] = s;
+        cidx[(size_t)pos[(size_t)gj]] = (int32_t)gi;
+        cval[(size_t)pos[(size_t)gj]++] = s;
+        sig[(size_t)gi] += s;
+        sig[(size_t)gj] += s;
+      } else if (!fa && fb) {
+        dbase[(size_t)gi] += s;
+        F[(size_t)gi] += s * c->hc[h.b].gfix[(size_t)h.j[e]];
+      } else if (fa && !fb) {
+        dbase[(size_t)gj] += s;
+        F[(size_t)gj] += s * c->hc[h.a].gfix[(size_t)h.i[e]];
+      }
+    }
+  std::vector<double> dsD((size_t)N, 0.0), dinv((size_t)N, 0.0);
+  for (int a = 0; a < c->L; ++a)
+    for (int64_t i = 0; i < c->hc[a].n; ++i) {
+      const size_t g = (size_t)(c->off[a] + i);
+      dsD[g] = dbase[g] + sig[g];
+      const double diag = dsD[g] + tsum[g];            // diag(K), Jacobi (reading C14)
+      if (!(diag > 0.0) || !std::isfinite(diag))
+        return fail(c, MC_ERR_ARG, "continuum %d row %lld: diagonal %g of M/tau + A is not > 0", a,
+                    (long long)i, diag);
+      dinv[g] = 1.0 / diag;
+    }
+  mc_status st;
+#define UP(dst, src) \
+  if ((st = upload(c, &(dst), (src))) != MC_OK) return st
+  UP(c->mtau, mtau);
+  UP(c->dsC, dbase);
+  UP(c->dsD, dsD);
+  UP(c->dinv, dinv);
+  UP(c->F, F);
+  UP(c->cptr, cnt);
+  UP(c->cidx, cidx);
+  UP(c->cval, cval);
+  UP(c->u[0], u0);
+  for (int a = 0; a < c->L; ++a) {
+    HostCont& H = c->hc[a];
+    if (H.kind == KIND_GRID) {
+      UP(c->Tx[a], H.Tx);
+      UP(c->Ty[a], H.Ty);
+    } else {
+      std::vector<int32_t> gcol(H.col);
+      for (auto& v : gcol) v += (int32_t)c->off[a];
+      UP(c->rowptr[a], H.rowptr);
+      UP(c->col[a], gcol);
+      if (!H.val.empty()) UP(c->val[a], H.val);
+    }
+  }
+#undef UP
+  for (int k = 0; k < 2; ++k) {
+    if (k == 1 && (st = dev_alloc(c, &c->u[1], (size_t)N)) != MC_OK) return st;
+    if ((st = dev_alloc(c, &c->r[k], (size_t)N)) != MC_OK) return st;
+    if ((st = dev_alloc(c, &c->p[k], (size_t)N)) != MC_OK) return st;
+    if ((st = dev_alloc(c, &c->q[k], (size_t)N)) != MC_OK) return st;
+    CUDA_TRY(c, cudaMemsetAsync(c->r[k], 0, (size_t)N * 8, c->stream));
+    CUDA_TRY(c, cudaMemsetAsync(c->p[k], 0, (size_t)N * 8, c->stream));
+    CUDA_TRY(c, cudaMemsetAsync(c->q[k], 0, (size_t)N * 8, c->stream));
+  }
+  CUDA_TRY(c, cudaMemcpyAsync(c->u[1], c->u[0], (size_t)N * 8, cudaMemcpyDeviceToDevice, c->stream));
+  if ((st = dev_alloc(c, &c->partials, (size_t)2 * kNPart * c->total_ctas)) != MC_OK) return st;
+  if ((st = dev_alloc(c, &c->sync, 1)) != MC_OK) return st;
+  if ((st = dev_alloc(c, &c->gout, MC_MAX_CONTINUA)) != MC_OK) return st;
+  if ((st = dev_alloc(c, &c->cur, 1)) != MC_OK) return st;
+  if ((st = dev_alloc(c, &c->fail, 1)) != MC_OK) return st;
+  if ((st = dev_alloc(c, &c->rep, 1)) != MC_OK) return st;
+  CUDA_TRY(c, cudaMemsetAsync(c->cur, 0, 4, c->stream));
+  CUDA_TRY(c, cudaMemsetAsync(c->fail, 0, 4, c->stream));
+  CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  c->cur_host = 0;
+  // host copies no longer needed
+  for (int a = 0; a < c->L; ++a) {
+    HostCont& H = c->hc[a];
+    std::vector<double>().swap(H.mtau);
+    std::vector<double>().swap(H.dbase);
+    std::vector<double>().swap(H.F);
+    std::vector<double>().swap(H.u0);
+    std::vector<double>().swap(H.tsum);
+    std::vector<double>().swap(H.Tx);
+    std::vector<double>().swap(H.Ty);
+    std::vector<int32_t>().swap(H.col);
+    std::vector<double>().swap(H.val);
+  }
+  c->cpl.clear();
+  c->finalized = true;
+  return MC_OK;
+}
+
+// ====================================================================== work plan
+static void add_items(const mc_ctx* c, int a, int warps, std::vector<Item>& items) {
+  const HostCont& H = c->hc[a];
+  warps = std::max(warps, 1);
+  if (H.kind == KIND_GRID) {
+    const int strips = (H.nx + 31) / 32;
+    const int segs = std::max(1, (warps + strips - 1) / strips);
+    const int hgt = std::max(1, (H.ny + segs - 1) / segs);
+    for (int s = 0; s < strips; ++s)
+      for (int y0 = 0; y0 < H.ny; y0 += hgt) {
+        Item it{};
+        it.cont = a;
+        it.kind = ITEM_GRID;
+        it.a = s * 32;
+        it.b = y0;
+        it.c = std::min(H.ny, y0 + hgt);
+        items.push_back(it);
+      }
+  } else {
+    int64_t chunk = (H.n + warps - 1) / warps;
+    chunk = std::max<int64_t>(32, (chunk + 31) / 32 * 32);
+    for (int64_t r0 = 0; r0 < H.n; r0 += chunk) {
+      Item it{};
+      it.cont = a;
+      it.kind = ITEM_GRAPH;
+      it.a = (int32_t)r0;
+      it.b = (int32_t)std::min<int64_t>(H.n, r0 + chunk);
+      items.push_back(it);
+    }
+  }
+}
+
+static int64_t default_maxit(const mc_ctx* c, int64_t n) {
+  if (c->opt.maxit > 0) return c->opt.maxit;
+  return std::min<int64_t>(10 * n, 2000000);
+}
+
+// CTAs a latency-bound solve of n rows can use with >= 2 rows per thread
+static int useful_ctas(int64_t n) { return (int)std::max<int64_t>(1, (n + 2 * kThreads - 1) / (2 * kThreads)); }
+
+static Plan make_plan(const mc_ctx* c, int scheme) {
+  Plan P;
+  const int T = c->total_ctas;
+  const double tol2 = c->opt.rtol * c->opt.rtol;
+  if (scheme == MC_COUPLED) {
+    P.ngroups = 1;
+    P.nphases = 1;
+    Group& g = P.grp[0];
+    g.cta_begin = 0;
+    g.cta_count = T;
+    g.phase = 0;
+    g.tol2 = tol2;
+    int64_t ntot = 0;
+    for (int a = 0; a < c->L; ++a) ntot += c->hc[a].n;
+    g.maxit = default_maxit(c, ntot);
+    g.cont_mask = (1 << c->L) - 1;
+    g.item_begin = 0;
+    for (int a = 0; a < c->L; ++a)
+      add_items(c, a, (int)std::max<int64_t>(1, (int64_t)T * kWarps * c->hc[a].n / ntot), P.items);
+    g.item_count = (int32_t)P.items.size();
+    P.valid = true;
+    return P;
+  }
+  const int L = c->L;
+  P.ngroups = L;
+  bool all_large = true, hist = true;
+  for (int a = 0; a < L; ++a) {
+    if (c->hc[a].n < kLargeRows) all_large = false;
+    if (c->last_iters[a] <= 0) hist = false;
+  }
+  int ctas[MC_MAX_CONTINUA] = {0};
+  if (all_large || !hist || L == 1) {
+    // sequential phases, every solve on all CTAs (bandwidth-bound, or no iteration history)
+    P.nphases = L;
+    for (int a = 0; a < L; ++a) {
+      P.grp[a].phase = a;
+      P.grp[a].cta_begin = 0;
+      ctas[a] = T;
+    }
+  } else {
+    // one phase: CTAs split by work (rows x last iterations), each solve guaranteed the
+    // CTAs its latency-bound loop can use (capped at an equal share)
+    P.nphases = 1;
+    double w[MC_MAX_CONTINUA], wsum = 0.0;
+    int used = 0;
+    for (int a = 0; a < L; ++a) {
+      w[a] = (double)c->hc[a].n * (double)c->last_iters[a];
+      wsum += w[a];
+      ctas[a] = std::min(useful_ctas(c->hc[a].n), std::max(1, T / (2 * L)));
+      used += ctas[a];
+    }
+    int rest = T - used;
+    int given = 0;
+    for (int a = 0; a < L; ++a) {
+      const int add = (int)std::floor(rest * (w[a] / wsum));
+      ctas[a] += add;
+      given += add;
+    }
+    int amax = 0;
+    for (int a = 1; a < L; ++a)
+      if (w[a] > w[amax]) amax = a;
+    ctas[amax] += rest - given;
+    int b = 0;
+    for (int a = 0; a < L; ++a) {
+      P.grp[a].phase = 0;
+      P.grp[a].cta_begin = b;
+      b += ctas[a];
+    }
+  }
+  for (int a = 0; a < L; ++a) {
+    Group& g = P.grp[a];
+    g.cta_count = ctas[a];
+    g.tol2 = tol2;
+    g.maxit = default_maxit(c, c->hc[a].n);
+    g.cont_mask = 1 << a;
+    g.item_begin = (int32_t)P.items.size();
+    add_items(c, a, ctas[a] * kWarps, P.items);
+    g.item_count = (int32_t)P.items.size() - g.item_begin;
+  }
+  P.valid = true;
+  return P;
+}
+
+static bool same_plan(const Plan& a, const Plan& b) {
+  if (!a.valid || !b.valid || a.ngroups != b.ngroups || a.nphases != b.nphases) return false;
+  for (int g = 0; g < a.ngroups; ++g)
+    if (a.grp[g].cta_begin != b.grp[g].cta_begin || a.grp[g].cta_count != b.grp[g].cta_count ||
+        a.grp[g].phase != b.grp[g].phase)
+      return false;
+  return true;
+}
+
+// ====================================================================== stepping
+static mc_status enqueue_step(mc_ctx* c, int scheme) {
+  Plan np = make_plan(c, scheme);
+  Plan& cp = c->plan[scheme];
+  if (!same_plan(np, cp) || c->uploaded_plan != scheme) {
+    cp = np;
+    if (cp.items.size() > c->items_cap) {
+      if (c->items) {
+        cudaStreamSynchronize(c->stream);
+        cudaFree(c->items);
+        c->allocs.erase(std::find(c->allocs.begin(), c->allocs.end(), (void*)c->items));
+        c->items = nullptr;
+      }
+      mc_status st = dev_alloc(c, &c->items, cp.items.size() * 2);
+      if (st != MC_OK) return st;
+      c->items_cap = cp.items.size() * 2;
+    }
+    CUDA_TRY(c, cudaMemcpyAsync(c->items, cp.items.data(), cp.items.size() * sizeof(Item),
+                                cudaMemcpyHostToDevice, c->stream));
+    c->uploaded_plan = scheme;
+  }
+  StepParams P{};
+  for (int a = 0; a < c->L; ++a) {
+    ContDev& C = P.cont[a];
+    const HostCont& H = c->hc[a];
+    C.kind = H.kind;
+    C.nx = H.nx;
+    C.ny = H.ny;
+    C.off = c->off[a];
+    C.n = H.n;
+    C.Tx = c->Tx[a];
+    C.Ty = c->Ty[a];
+    C.rowptr = c->rowptr[a];
+    C.col = c->col[a];
+    C.val = c->val[a];
+    C.Tconst = H.Tconst;
+  }
+  for (int g = 0; g < cp.ngroups; ++g) P.grp[g] = cp.grp[g];
+  P.L = c->L;
+  P.ngroups = cp.ngroups;
+  P.nphases = cp.nphases;
+  P.coupled = (scheme == MC_COUPLED);
+  P.total_ctas = c->total_ctas;
+  P.N = c->N;
+  for (int k = 0; k < 2; ++k) {
+    P.u[k] = c->u[k];
+    P.r[k] = c->r[k];
+    P.p[k] = c->p[k];
+    P.q[k] = c->q[k];
+  }
+  P.dinv = c->dinv;
+  P.dsD = c->dsD;
+  P.dsC = c->dsC;
+  P.mtau = c->mtau;
+  P.F = c->F;
+  P.cptr = c->cptr;
+  P.cidx = c->cidx;
+  P.cval = c->cval;
+  P.items = c->items;
+  P.partials = c->partials;
+  P.sync = c->sync;
+  P.gout = c->gout;
+  P.cur = c->cur;
+  P.fail = c->fail;
+  P.rep = c->rep;
+  P.step_no = c->step_no + 1;
+  P.scheme = scheme;
+  CUDA_TRY(c, cudaMemsetAsync(c->sync, 0, sizeof(SyncBlock), c->stream));
+  CUDA_TRY(c, cudaEventRecord(c->ev0, c->stream));
+  CUDA_TRY(c, launch_step(&P, c->total_ctas, c->stream));
+  CUDA_TRY(c, cudaEventRecord(c->ev1, c->stream));
+  return MC_OK;
+}
+
+// wait for the step, read its report, update host mirrors
+static mc_status complete_step(mc_ctx* c, int scheme, mc_step_report* out) {
+  CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  mc_step_report rep;
+  CUDA_TRY(c, cudaMemcpy(&rep, c->rep, sizeof rep, cudaMemcpyDeviceToHost));
+  float ms = 0.f;
+  CUDA_TRY(c, cudaEventElapsedTime(&ms, c->ev0, c->ev1));
+  rep.ms = ms;
+  if (rep.status == MC_OK) {
+    c->cur_host ^= 1;
+    c->step_no += 1;
+    if (scheme == MC_DECOUPLED_D)
+      for (int a = 0; a < c->L; ++a) c->last_iters[a] = rep.iters[a];
+  }
+  if (out) *out = rep;
+  if (rep.status != MC_OK) {
+    const char* what = rep.status == MC_ERR_NOCONV ? "no convergence within maxit"
+                       : rep.status == MC_ERR_BREAKDOWN ? "CG breakdown (p.q <= 0)"
+                                                        : "step skipped after an earlier failure";
+    return fail(c, (mc_status)rep.status, "step %d (%s), solve %d: %s after %lld iterations; state not advanced",
+                c->step_no + 1, scheme == MC_COUPLED ? "coupled" : "D-scheme", rep.failed_solve, what,
+                rep.failed_solve >= 0 ? (long long)rep.iters[rep.failed_solve] : 0LL);
+  }
+  return MC_OK;
+}
+
+static mc_status do_step(mc_ctx* c, int scheme, mc_step_report* rep) {
+  if (!c) return fail(c, MC_ERR_ARG, "NULL context");
+  mc_status st = finalize(c);
+  if (st != MC_OK) return st;
+  CUDA_TRY(c, cudaMemsetAsync(c->fail, 0, 4, c->stream));
+  if ((st = enqueue_step(c, scheme)) != MC_OK) return st;
+  return complete_step(c, scheme, rep);
+}
+
+extern "C" mc_status mc_step_decoupled(mc_ctx* c, mc_step_report* rep) {
+  return do_step(c, MC_DECOUPLED_D, rep);
+}
+
+extern "C" mc_status mc_step_coupled(mc_ctx* c, mc_step_report* rep) {
+  return do_step(c, MC_COUPLED, rep);
+}
+
+extern "C" mc_status mc_run(mc_ctx* c, int32_t scheme, int32_t n_steps, mc_step_report* reps,
+                            double* const* snapshots) {
+  if (!c) return fail(c, MC_ERR_ARG, "NULL context");
+  if (scheme != MC_COUPLED && scheme != MC_DECOUPLED_D) return fail(c, MC_ERR_ARG, "unknown scheme %d", scheme);
+  if (n_steps < 0) return fail(c, MC_ERR_ARG, "n_steps < 0");
+  mc_status st = finalize(c);
+  if (st != MC_OK) return st;
+  for (int32_t s = 0; s < n_steps; ++s) {
+    mc_step_report rep;
+    st = do_step(c, scheme, &rep);
+    if (reps) reps[s] = rep;
+    if (st != MC_OK) {
+      for (int32_t t = s + 1; t < n_steps && reps; ++t) {
+        std::memset(&reps[t], 0, sizeof(mc_step_report));
+        reps[t].status = MC_ERR_STATE;
+        reps[t].failed_solve = -1;
+      }
+      return st;
+    }
+    if (snapshots)
+      for (int a = 0; a < c->L; ++a) {
+        double* dst = snapshots[(size_t)s * c->L + a];
+        if (dst)
+          CUDA_TRY(c, cudaMemcpyAsync(dst, c->u[c->cur_host] + c->off[a], (size_t)c->hc[a].n * 8,
+                                      cudaMemcpyDefault, c->stream));
+      }
+  }
+  CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  return MC_OK;
+}
+
+extern "C" mc_status mc_get_state(mc_ctx* c, int32_t alpha, double* dst) {
+  if (!c || !dst) return fail(c, MC_ERR_ARG, "NULL argument");
+  if (alpha < 0 || alpha >= c->L) return fail(c, MC_ERR_ARG, "alpha = %d out of range", alpha);
+  mc_status st = finalize(c);
+  if (st != MC_OK) return st;
+  CUDA_TRY(c, cudaMemcpyAsync(dst, c->u[c->cur_host] + c->off[alpha], (size_t)c->hc[alpha].n * 8,
+                              cudaMemcpyDefault, c->stream));
+  CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  return MC_OK;
+}
+
+extern "C" mc_status mc_set_state(mc_ctx* c, int32_t alpha, const double* src) {
+  if (!c || !src) return fail(c, MC_ERR_ARG, "NULL argument");
+  if (alpha < 0 || alpha >= c->L) return fail(c, MC_ERR_ARG, "alpha = %d out of range", alpha);
+  mc_status st = finalize(c);
+  if (st != MC_OK) return st;
+  CUDA_TRY(c, cudaMemcpyAsync(c->u[c->cur_host] + c->off[alpha], src, (size_t)c->hc[alpha].n * 8,
+                              cudaMemcpyDefault, c->stream));
+  CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  return MC_OK;
+}
+
+extern "C" mc_status mc_last_kernel_ms(mc_ctx* c, double* ms_out) {
+  if (!c || !ms_out) return fail(c, MC_ERR_ARG, "NULL argument");
+  float ms = 0.f;
+  CUDA_TRY(c, cudaEventElapsedTime(&ms, c->ev0, c->ev1));
+  *ms_out = ms;
+  return MC_OK;
+}

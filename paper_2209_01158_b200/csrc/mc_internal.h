@@ -1,0 +1,100 @@
+// mc_internal.h — structures shared by the host API (mc_api.cu) and the sm_100a
+// kernels (mc_kernels.cu).  Not part of the public ABI (include/mc.h).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+#include "../../include/mc.h"
+
+namespace mc {
+
+constexpr int kThreads = 256;          // threads per CTA of the step kernel
+constexpr int kWarps = kThreads / 32;
+constexpr int kMinBlocks = 4;          // __launch_bounds__ residency target (4 x 256 per SM)
+constexpr int kNPart = 5;              // reduction slots per barrier (pq, rr, rz, rq, qq)
+constexpr int kPadDofs = 32;           // continuum offsets padded to 32 doubles (256 B)
+
+enum ContKind : int32_t { KIND_GRID = 0, KIND_GRAPH = 1 };
+enum ItemKind : int32_t { ITEM_GRID = 0, ITEM_GRAPH = 1 };
+
+// one continuum as the kernels see it
+struct ContDev {
+  int32_t kind;
+  int32_t nx, ny;          // grid
+  int64_t off, n;          // global DOF offset and count
+  const double* Tx;        // grid: face (iy,ix)-(iy,ix+1); 0 on the last column
+  const double* Ty;        // grid: face (iy,ix)-(iy+1,ix); 0 on the last row
+  const int32_t* rowptr;   // graph: [n+1], local
+  const int32_t* col;      // graph: GLOBAL column indices
+  const double* val;       // graph: per-entry T, or nullptr -> Tconst
+  double Tconst;
+};
+
+// a work item: a 32-column strip segment of a grid, or a row range of a graph
+struct Item {
+  int32_t cont;
+  int32_t kind;
+  int32_t a, b, c;         // grid: x0, y0, y1   graph: r0, r1, -
+  int32_t pad;
+};
+
+// one CG solve (D-scheme: one continuum; coupled: all)
+struct Group {
+  int32_t cta_begin, cta_count;
+  int32_t item_begin, item_count;
+  int64_t maxit;
+  double tol2;             // rtol^2
+  int32_t cont_mask;       // continua solved by this group
+  int32_t phase;           // groups of one phase run concurrently; phases run in order
+};
+
+// per-group device results of one step
+struct GroupOut {
+  int64_t iters;
+  int32_t status;          // mc_status
+  int32_t pad;
+  double bb, rr;           // ||b||^2, final ||r||^2
+  long long t0, t1;        // %globaltimer ns
+};
+
+struct SyncBlock {         // zeroed before every step launch
+  unsigned long long arrive[MC_MAX_CONTINUA];
+  unsigned long long phase_arrive;
+  unsigned int finished;
+  unsigned int pad[3];
+};
+
+struct StepParams {
+  ContDev cont[MC_MAX_CONTINUA];
+  Group grp[MC_MAX_CONTINUA];
+  int32_t L, ngroups, nphases, coupled, total_ctas;
+  int64_t N;               // padded global size
+  // state and CG work vectors (global DOF space, padded)
+  double* u[2];            // ping-pong state: u[cur] = p^{n-1}, u[cur^1] = iterate x
+  double* r[2];
+  double* p[2];
+  double* q[2];
+  // operator data
+  const double* dinv;      // 1 / diag(K) (Jacobi; identical for both schemes, reading C14)
+  const double* dsD;       // D-scheme shift  m/tau + boundary + sum_b sigma
+  const double* dsC;       // coupled shift   m/tau + boundary
+  const double* mtau;      // m / tau
+  const double* F;         // time-constant source incl. Dirichlet terms
+  const int32_t* cptr;     // coupling CSR over global rows [N+1]
+  const int32_t* cidx;     // global column
+  const double* cval;      // sigma
+  const Item* items;
+  double* partials;        // [2][kNPart][total_ctas]
+  SyncBlock* sync;
+  GroupOut* gout;          // [ngroups]
+  int32_t* cur;            // device ping-pong index
+  int32_t* fail;           // sticky failure flag (mc_run)
+  mc_step_report* rep;     // report slot of this launch
+  int32_t step_no;
+  int32_t scheme;
+};
+
+// kernel launch (mc_kernels.cu)
+cudaError_t launch_step(const StepParams* dparams, int total_ctas, cudaStream_t s);
+cudaError_t step_kernel_occupancy(int* blocks_per_sm);
+
+}  // namespace mc

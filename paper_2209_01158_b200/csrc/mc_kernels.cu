@@ -1,0 +1,480 @@
+// mc_kernels.cu — the sm_100a step kernel of libmc.
+//
+// One persistent, cooperatively launched kernel advances the whole system by one time
+// layer.  Its CTAs are partitioned into groups; each group runs one
+// Jacobi-preconditioned CG solve:
+//   D-scheme: one group per continuum, all groups concurrently; the
+//            inter-continuum transfer enters only the right-hand side, from layer n-1.
+//   coupled: one group over all continua, transfer in the operator.
+//
+// Per step:   init pass   b = (m/tau) u^{n-1} + F [+ sum_b Q_ab u_b^{n-1}],  r0 = b - K x0,
+//                         x0 = u^{n-1} (warm start);  one group reduction.
+//             CG passes   one fused pass and ONE group reduction per iteration:
+//                         r_j = r_{j-1} - a q_{j-1};  x_j = x_{j-1} + a p_{j-1};
+//                         p_j = D^{-1} r_j + b p_{j-1};  q_j = K p_j;
+//                         partials (p.q, r.r, r.z, z.q, q.D^{-1}q) -> a = (r.z)/(p.q),
+//                         (r.z)_{j+1} = r.z - 2a z.q + a^2 q.D^{-1}q,  b = (r.z)_{j+1}/(r.z).
+//   This is CG in exact arithmetic with the recursive residual computed exactly
+//   (reading C13 stop rule), reorganised so each iteration reads every vector once
+//   (single-reduction form).  Neighbour values of p_j needed by the
+//   SpMV are recomputed from r, q, p of the previous iteration (bitwise identical
+//   to what the owner stores), so no barrier separates the update from the SpMV.
+//
+// Operators (flux form, reading C15):
+//   grid: q_i = ds_i p_i + sum_faces T_f (p_i - p_nb)
+//   graph: q_i = ds_i p_i + sum_e T_e (p_i - p_j)
+//   coupled adds sum_cpl sigma (p_i - p_other).
+#include "mc_internal.h"
+
+namespace mc {
+
+__device__ __forceinline__ double ldro(const double* p) { return __ldg(p); }
+__device__ __forceinline__ int32_t ldro(const int32_t* p) { return __ldg(p); }
+__device__ __forceinline__ double ldmut(const double* p) { return __ldcg(p); }
+__device__ __forceinline__ void stmut(double* p, double v) { __stcg(p, v); }
+
+__device__ __forceinline__ unsigned long long ld_acquire(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__device__ __forceinline__ long long globaltimer() {
+  long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+// p_j = D^{-1}(r_{j-1} - a q_{j-1}) + b p_{j-1}; one definition used by owners and by
+// neighbours so the recomputed halo value is bitwise identical to the stored one.
+__device__ __forceinline__ double pnew(double ro, double qo, double po, double di, double a,
+                                       double b) {
+  const double rn = __fma_rn(-a, qo, ro);
+  return __fma_rn(di, rn, __dmul_rn(b, po));
+}
+
+struct Ctx {
+  const StepParams* P;
+  const double* rs;
+  const double* qs;
+  const double* ps;
+  double* rd;
+  double* pd;
+  double* qd;
+  double* x;
+  const double* ds;
+  double a, b;
+
+  __device__ __forceinline__ double pn_at(int64_t gi) const {
+    return pnew(ldmut(rs + gi), ldmut(qs + gi), ldmut(ps + gi), ldro(P->dinv + gi), a, b);
+  }
+  // owner update of row gi: x, r, p stored; returns p_j, r_j, D^{-1}_ii
+  __device__ __forceinline__ void own(int64_t gi, double& pn, double& rn, double& di) const {
+    const double ro = ldmut(rs + gi), qo = ldmut(qs + gi), po = ldmut(ps + gi);
+    di = ldro(P->dinv + gi);
+    const double xo = x[gi];
+    rn = __fma_rn(-a, qo, ro);
+    pn = __fma_rn(di, rn, __dmul_rn(b, po));
+    x[gi] = __fma_rn(a, po, xo);
+    stmut(rd + gi, rn);
+    stmut(pd + gi, pn);
+  }
+  __device__ __forceinline__ double couple_q(int64_t gi, double pc) const {
+    double acc = 0.0;
+    const int32_t e0 = ldro(P->cptr + gi), e1 = ldro(P->cptr + gi + 1);
+    for (int32_t e = e0; e < e1; ++e) {
+      const int32_t j = ldro(P->cidx + e);
+      acc += ldro(P->cval + e) * (pc - pn_at(j));
+    }
+    return acc;
+  }
+  __device__ __forceinline__ void accum(double (&acc)[kNPart], double pc, double rc, double dc,
+                                        double qv) const {
+    acc[0] += pc * qv;        // p.q
+    acc[1] += rc * rc;        // r.r   (exact recursive residual norm)
+    acc[2] += dc * rc * rc;   // r.z   (z = D^{-1} r)
+    acc[3] += dc * rc * qv;   // z.q
+    acc[4] += dc * qv * qv;   // q.D^{-1}q
+  }
+};
+
+// ---------------------------------------------------------------- CG pass, grid strip
+template <bool CPL>
+__device__ void iter_grid(const Ctx& c, const ContDev& C, int x0, int y0, int y1,
+                          double (&acc)[kNPart]) {
+  const int lane = threadIdx.x & 31;
+  const int nx = C.nx, ny = C.ny;
+  const int col = x0 + lane;
+  const bool valid = col < nx;
+  const int64_t off = C.off;
+  double pm = 0.0, tym = 0.0;
+  if (valid && y0 > 0) {
+    const int64_t i = (int64_t)(y0 - 1) * nx + col;
+    pm = c.pn_at(off + i);
+    tym = ldro(C.Ty + i);
+  }
+  double pc = 0.0, rc = 0.0, dc = 0.0;
+  if (valid) c.own(off + (int64_t)y0 * nx + col, pc, rc, dc);
+  for (int y = y0; y < y1; ++y) {
+    const int64_t i = (int64_t)y * nx + col;
+    const int64_t gi = off + i;
+    double pp = 0.0, rp = 0.0, dp = 0.0;
+    if (valid && y + 1 < ny) {
+      if (y + 1 < y1) c.own(gi + nx, pp, rp, dp);
+      else pp = c.pn_at(gi + nx);
+    }
+    const double txc = valid ? ldro(C.Tx + i) : 0.0;
+    double pl = __shfl_up_sync(0xffffffffu, pc, 1);
+    double pr = __shfl_down_sync(0xffffffffu, pc, 1);
+    double txl = __shfl_up_sync(0xffffffffu, txc, 1);
+    if (lane == 0) {
+      if (valid && col > 0) {
+        pl = c.pn_at(gi - 1);
+        txl = ldro(C.Tx + i - 1);
+      } else {
+        pl = 0.0;
+        txl = 0.0;
+      }
+    }
+    if (lane == 31) pr = (valid && col + 1 < nx) ? c.pn_at(gi + 1) : 0.0;
+    if (valid) {
+      const double tyc = ldro(C.Ty + i);
+      double qv = ldro(c.ds + gi) * pc;
+      qv += txc * (pc - pr);
+      qv += txl * (pc - pl);
+      qv += tyc * (pc - pp);
+      qv += tym * (pc - pm);
+      if (CPL) qv += c.couple_q(gi, pc);
+      stmut(c.qd + gi, qv);
+      c.accum(acc, pc, rc, dc, qv);
+      tym = tyc;
+    }
+    pm = pc;
+    pc = pp;
+    rc = rp;
+    dc = dp;
+  }
+}
+
+// ---------------------------------------------------------------- CG pass, graph rows
+template <bool CPL>
+__device__ void iter_graph(const Ctx& c, const ContDev& C, int r0, int r1,
+                           double (&acc)[kNPart]) {
+  const int lane = threadIdx.x & 31;
+  for (int i = r0 + lane; i < r1; i += 32) {
+    const int64_t gi = C.off + i;
+    double pc, rc, dc;
+    c.own(gi, pc, rc, dc);
+    double qv = ldro(c.ds + gi) * pc;
+    const int32_t e0 = ldro(C.rowptr + i), e1 = ldro(C.rowptr + i + 1);
+    if (C.val) {
+      for (int32_t e = e0; e < e1; ++e) qv += ldro(C.val + e) * (pc - c.pn_at(ldro(C.col + e)));
+    } else {
+      double s = 0.0;
+      for (int32_t e = e0; e < e1; ++e) s += pc - c.pn_at(ldro(C.col + e));
+      qv += C.Tconst * s;
+    }
+    if (CPL) qv += c.couple_q(gi, pc);
+    stmut(c.qd + gi, qv);
+    c.accum(acc, pc, rc, dc, qv);
+  }
+}
+
+// ---------------------------------------------------------------- init pass
+// b = (m/tau) u + F + [D: sum sigma u_other];  r0 = b - K u;  x = u;  p0 = q0 = 0
+template <bool CPL>
+__device__ __forceinline__ void init_row(const StepParams& P, int64_t gi, double Ku_nb,
+                                         const double* uo, double* x, double (&acc)[3]) {
+  const double u = uo[gi];
+  double b = ldro(P.mtau + gi) * u + ldro(P.F + gi);
+  double Ku = ldro((CPL ? P.dsC : P.dsD) + gi) * u + Ku_nb;
+  const int32_t e0 = ldro(P.cptr + gi), e1 = ldro(P.cptr + gi + 1);
+  for (int32_t e = e0; e < e1; ++e) {
+    const int32_t j = ldro(P.cidx + e);
+    const double s = ldro(P.cval + e);
+    if (CPL) Ku += s * (u - uo[j]);
+    else b += s * uo[j];     // lagged transfer Q_ab u_b^{n-1}
+  }
+  const double r = b - Ku;
+  x[gi] = u;
+  stmut(P.r[0] + gi, r);
+  stmut(P.p[0] + gi, 0.0);
+  stmut(P.q[0] + gi, 0.0);
+  acc[0] += b * b;
+  acc[1] += r * r;
+  acc[2] += ldro(P.dinv + gi) * r * r;
+}
+
+template <bool CPL>
+__device__ void init_item(const StepParams& P, const Item& it, const double* uo, double* x,
+                          double (&acc)[3]) {
+  const ContDev& C = P.cont[it.cont];
+  const int lane = threadIdx.x & 31;
+  if (it.kind == ITEM_GRID) {
+    const int nx = C.nx, ny = C.ny, col = it.a + lane;
+    if (col >= nx) return;
+    for (int y = it.b; y < it.c; ++y) {
+      const int64_t i = (int64_t)y * nx + col, gi = C.off + i;
+      const double u = uo[gi];
+      double s = 0.0;
+      if (col > 0) s += ldro(C.Tx + i - 1) * (u - uo[gi - 1]);
+      if (col + 1 < nx) s += ldro(C.Tx + i) * (u - uo[gi + 1]);
+      if (y > 0) s += ldro(C.Ty + i - nx) * (u - uo[gi - nx]);
+      if (y + 1 < ny) s += ldro(C.Ty + i) * (u - uo[gi + nx]);
+      init_row<CPL>(P, gi, s, uo, x, acc);
+    }
+  } else {
+    for (int i = it.a + lane; i < it.b; i += 32) {
+      const int64_t gi = C.off + i;
+      const double u = uo[gi];
+      const int32_t e0 = ldro(C.rowptr + i), e1 = ldro(C.rowptr + i + 1);
+      double s = 0.0;
+      for (int32_t e = e0; e < e1; ++e) {
+        const double t = C.val ? ldro(C.val + e) : C.Tconst;
+        s += t * (u - uo[ldro(C.col + e)]);
+      }
+      init_row<CPL>(P, gi, s, uo, x, acc);
+    }
+  }
+}
+
+__device__ void zero_item(const StepParams& P, const Item& it, double* x) {
+  const ContDev& C = P.cont[it.cont];
+  const int lane = threadIdx.x & 31;
+  if (it.kind == ITEM_GRID) {
+    const int col = it.a + lane;
+    if (col >= C.nx) return;
+    for (int y = it.b; y < it.c; ++y) x[C.off + (int64_t)y * C.nx + col] = 0.0;
+  } else {
+    for (int i = it.a + lane; i < it.b; i += 32) x[C.off + i] = 0.0;
+  }
+}
+
+// ---------------------------------------------------------------- group all-reduce + barrier
+// Deterministic: CTA partial = fixed-order warp/CTA tree; group total = fixed-order sum
+// over the group's CTAs, computed redundantly (identically) by every CTA of the group.
+template <int NP>
+__device__ __forceinline__ void group_allreduce(const StepParams& P, int g, int cl,
+                                                unsigned long long& epoch, const double (&v)[NP],
+                                                double (&out)[NP]) {
+  __shared__ double sh[kWarps][kNPart];
+  __shared__ double tot[kNPart];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int G = P.grp[g].cta_count, base = P.grp[g].cta_begin;
+#pragma unroll
+  for (int k = 0; k < NP; ++k) {
+    double s = v[k];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) sh[w][k] = s;
+  }
+  __syncthreads();
+  double* part = P.partials + (size_t)(epoch & 1ull) * kNPart * P.total_ctas;
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int k = 0; k < NP; ++k) {
+      double s = 0.0;
+#pragma unroll
+      for (int i = 0; i < kWarps; ++i) s += sh[i][k];
+      __stcg(part + (size_t)k * P.total_ctas + base + cl, s);
+    }
+    __threadfence();
+    unsigned long long* ctr = &P.sync->arrive[g];
+    atomicAdd(ctr, 1ull);
+    const unsigned long long target = (epoch + 1ull) * (unsigned long long)G;
+    while (ld_acquire(ctr) < target) {
+    }
+    __threadfence();
+  }
+  __syncthreads();
+  if (w < NP) {
+    double s = 0.0;
+    const double* src = part + (size_t)w * P.total_ctas + base;
+    for (int i = lane; i < G; i += 32) s += __ldcg(src + i);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) tot[w] = s;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int k = 0; k < NP; ++k) out[k] = tot[k];
+  __syncthreads();
+  ++epoch;
+}
+
+// ---------------------------------------------------------------- the step kernel
+template <bool CPL>
+__device__ void run_group(const StepParams& P, int g, int cl, double* x, const double* uo) {
+  const Group& G = P.grp[g];
+  const int W = G.cta_count * kWarps;
+  const int wg = cl * kWarps + (threadIdx.x >> 5);
+  const int ib = G.item_begin, ie = G.item_begin + G.item_count;
+  const bool leader = (cl == 0 && threadIdx.x == 0);
+  long long t0 = leader ? globaltimer() : 0;
+
+  double a3[3] = {0.0, 0.0, 0.0};
+  for (int it = ib + wg; it < ie; it += W) init_item<CPL>(P, P.items[it], uo, x, a3);
+  unsigned long long epoch = 0;
+  double t3[3];
+  group_allreduce<3>(P, g, cl, epoch, a3, t3);
+  const double bb = t3[0];
+  double rr = t3[1];
+  int64_t iters = 0;
+  int status = MC_OK;
+  bool zero = false;
+  if (bb == 0.0) {
+    zero = true;       // b = 0  =>  x = 0 after 0 iterations
+    rr = 0.0;
+  } else if (!(rr <= G.tol2 * bb)) {
+    Ctx c;
+    c.P = &P;
+    c.x = x;
+    c.ds = CPL ? P.dsC : P.dsD;
+    c.a = 0.0;
+    c.b = 0.0;
+    for (int64_t j = 0;; ++j) {
+      const int s = (int)(j & 1);
+      c.rs = P.r[s];
+      c.qs = P.q[s];
+      c.ps = P.p[s];
+      c.rd = P.r[s ^ 1];
+      c.pd = P.p[s ^ 1];
+      c.qd = P.q[s ^ 1];
+      double a5[kNPart] = {0.0, 0.0, 0.0, 0.0, 0.0};
+      for (int it = ib + wg; it < ie; it += W) {
+        const Item item = P.items[it];
+        const ContDev& C = P.cont[item.cont];
+        if (item.kind == ITEM_GRID) iter_grid<CPL>(c, C, item.a, item.b, item.c, a5);
+        else iter_graph<CPL>(c, C, item.a, item.b, a5);
+      }
+      double t5[kNPart];
+      group_allreduce<kNPart>(P, g, cl, epoch, a5, t5);
+      rr = t5[1];
+      if (j > 0 && rr <= G.tol2 * bb) {
+        iters = j;
+        break;
+      }
+      if (j >= G.maxit) {
+        iters = j;
+        status = MC_ERR_NOCONV;
+        break;
+      }
+      if (!(t5[0] > 0.0) || !(t5[2] > 0.0)) {
+        iters = j;
+        status = MC_ERR_BREAKDOWN;
+        break;
+      }
+      const double rz = t5[2];
+      const double alpha = rz / t5[0];
+      const double rz_next = __fma_rn(alpha * alpha, t5[4], __fma_rn(-2.0 * alpha, t5[3], rz));
+      c.a = alpha;
+      c.b = rz_next / rz;
+    }
+  }
+  if (zero)
+    for (int it = ib + wg; it < ie; it += W) zero_item(P, P.items[it], x);
+  if (leader) {
+    GroupOut o;
+    o.iters = iters;
+    o.status = status;
+    o.pad = 0;
+    o.bb = bb;
+    o.rr = rr;
+    o.t0 = t0;
+    o.t1 = globaltimer();
+    P.gout[g] = o;
+  }
+}
+
+__device__ __forceinline__ void grid_barrier(const StepParams& P, unsigned long long target) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    atomicAdd(&P.sync->phase_arrive, 1ull);
+    while (ld_acquire(&P.sync->phase_arrive) < target) {
+    }
+    __threadfence();
+  }
+  __syncthreads();
+}
+
+__global__ void __launch_bounds__(kThreads, kMinBlocks) step_kernel(const __grid_constant__ StepParams P) {
+  const int failed = *(volatile const int32_t*)P.fail;
+  const int cur = *(volatile const int32_t*)P.cur;
+  if (!failed) {
+    const double* uo = P.u[cur];
+    double* x = P.u[cur ^ 1];
+    for (int ph = 0; ph < P.nphases; ++ph) {
+      for (int g = 0; g < P.ngroups; ++g) {
+        const Group& G = P.grp[g];
+        if (G.phase != ph || (int)blockIdx.x < G.cta_begin || (int)blockIdx.x >= G.cta_begin + G.cta_count)
+          continue;
+        const int cl = (int)blockIdx.x - G.cta_begin;
+        if (P.coupled) run_group<true>(P, g, cl, x, uo);
+        else run_group<false>(P, g, cl, x, uo);
+      }
+      if (ph + 1 < P.nphases) grid_barrier(P, (unsigned long long)(ph + 1) * gridDim.x);
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    const unsigned prev = atomicAdd(&P.sync->finished, 1u);
+    if (prev == gridDim.x - 1) {
+      __threadfence();
+      mc_step_report* rep = P.rep;
+      rep->step = P.step_no;
+      rep->scheme = P.scheme;
+      rep->nsolves = P.ngroups;
+      rep->failed_solve = -1;
+      rep->pad = 0;
+      if (failed) {
+        rep->status = MC_ERR_STATE;    // an earlier step of this run failed: skipped
+        for (int k = 0; k < MC_MAX_CONTINUA; ++k) {
+          rep->iters[k] = 0;
+          rep->relres[k] = 0.0;
+          rep->bnorm[k] = 0.0;
+          rep->ms_solve[k] = 0.0;
+        }
+      } else {
+        int st = MC_OK;
+        for (int k = 0; k < MC_MAX_CONTINUA; ++k) {
+          if (k < P.ngroups) {
+            volatile GroupOut* o = P.gout + k;
+            rep->iters[k] = o->iters;
+            const double bb = o->bb, rr = o->rr;
+            rep->bnorm[k] = sqrt(bb);
+            rep->relres[k] = bb > 0.0 ? sqrt(rr / bb) : 0.0;
+            rep->ms_solve[k] = (double)(o->t1 - o->t0) * 1e-6;
+            if (o->status != MC_OK && st == MC_OK) {
+              st = o->status;
+              rep->failed_solve = k;
+            }
+          } else {
+            rep->iters[k] = 0;
+            rep->relres[k] = 0.0;
+            rep->bnorm[k] = 0.0;
+            rep->ms_solve[k] = 0.0;
+          }
+        }
+        rep->status = st;
+        if (st == MC_OK) *(volatile int32_t*)P.cur = cur ^ 1;   // commit p^n (all solves converged)
+        else *(volatile int32_t*)P.fail = 1;
+      }
+      rep->ms = 0.0;
+      __threadfence();
+    }
+  }
+}
+
+cudaError_t launch_step(const StepParams* params, int total_ctas, cudaStream_t s) {
+  void* args[] = {(void*)params};
+  return cudaLaunchCooperativeKernel((const void*)step_kernel, dim3(total_ctas), dim3(kThreads),
+                                     args, 0, s);
+}
+
+cudaError_t step_kernel_occupancy(int* blocks_per_sm) {
+  return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, step_kernel, kThreads, 0);
+}
+
+}  // namespace mc

@@ -1,0 +1,282 @@
+"""Thin ctypes binding of libmc (include/mc.h) — argument marshalling only.
+
+Every step of the hot path runs in the sm_100a kernels of ``csrc/``; this module
+only mirrors the C structs, loads ``libmc.so`` (failing loudly if it is missing —
+there is no CPU fallback) and converts a generator scenario (``inputs/``) into
+the ABI's physical-input descriptors.  PyTorch provides device memory and the
+CUDA stream.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libmc.so")
+
+MC_OK, MC_ERR_ARG, MC_ERR_STATE, MC_ERR_NOMEM, MC_ERR_CUDA, MC_ERR_NOCONV, MC_ERR_BREAKDOWN = range(7)
+MC_GRID2D, MC_GRAPH = 0, 1
+MC_COUPLED, MC_DECOUPLED_D = 0, 1
+MC_MAX_CONTINUA = 4
+STATUS_NAMES = {0: "MC_OK", 1: "MC_ERR_ARG", 2: "MC_ERR_STATE", 3: "MC_ERR_NOMEM", 4: "MC_ERR_CUDA",
+                5: "MC_ERR_NOCONV", 6: "MC_ERR_BREAKDOWN"}
+
+_d = C.c_double
+_i32 = C.c_int32
+_i64 = C.c_int64
+_pd = C.POINTER(C.c_double)
+_pi = C.POINTER(C.c_int32)
+
+
+class mc_options(C.Structure):
+    _fields_ = [("tau", _d), ("rtol", _d), ("maxit", _i64), ("ctas", _i32), ("device", _i32),
+                ("stream", C.c_void_p)]
+
+
+class mc_continuum_desc(C.Structure):
+    _fields_ = [("kind", _i32), ("n", _i64),
+                ("c", _pd), ("c_const", _d), ("k", _pd), ("k_const", _d), ("f", _pd), ("u0", _pd),
+                ("nx", _i32), ("ny", _i32), ("h", _d), ("bc_left", _i32), ("bc_right", _i32),
+                ("g_left", _d), ("g_right", _d),
+                ("measure", _pd), ("measure_const", _d), ("n_edges", _i64), ("edge_i", _pi),
+                ("edge_j", _pi), ("edge_t", _pd), ("edge_geom", _d), ("dirichlet", _pd)]
+
+
+class mc_coupling_desc(C.Structure):
+    _fields_ = [("a", _i32), ("b", _i32), ("nnz", _i64), ("i_a", _pi), ("j_b", _pi), ("sigma", _pd),
+                ("sigma_const", _d), ("scale_by_measure", _i32)]
+
+
+class mc_step_report(C.Structure):
+    _fields_ = [("step", _i32), ("scheme", _i32), ("nsolves", _i32), ("status", _i32),
+                ("failed_solve", _i32), ("pad", _i32), ("iters", _i64 * MC_MAX_CONTINUA),
+                ("relres", _d * MC_MAX_CONTINUA), ("bnorm", _d * MC_MAX_CONTINUA),
+                ("ms_solve", _d * MC_MAX_CONTINUA), ("ms", _d)]
+
+    def as_dict(self):
+        k = self.nsolves
+        return dict(step=self.step, scheme=self.scheme, status=self.status, failed_solve=self.failed_solve,
+                    iters=list(self.iters[:k]), relres=list(self.relres[:k]), bnorm=list(self.bnorm[:k]),
+                    ms_solve=list(self.ms_solve[:k]), ms=self.ms)
+
+
+EXPORTS = ["mc_create", "mc_set_continuum", "mc_set_coupling", "mc_step_decoupled", "mc_step_coupled",
+           "mc_run", "mc_get_state", "mc_set_state", "mc_size", "mc_last_kernel_ms", "mc_destroy",
+           "mc_error_string", "mc_abi_version"]
+
+_lib = None
+
+
+def load(path: str = LIB_PATH):
+    """Load libmc.so; raises (no fallback) when it has not been built."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise RuntimeError(f"libmc.so not found at {path}: build it with "
+                           "`python -m paper_2209_01158_b200.build` (there is no CPU fallback)")
+    lib = C.CDLL(path)
+    P = C.c_void_p
+    lib.mc_create.argtypes = [C.POINTER(P), _i32, C.POINTER(mc_options)]
+    lib.mc_set_continuum.argtypes = [P, _i32, C.POINTER(mc_continuum_desc)]
+    lib.mc_set_coupling.argtypes = [P, C.POINTER(mc_coupling_desc)]
+    lib.mc_step_decoupled.argtypes = [P, C.POINTER(mc_step_report)]
+    lib.mc_step_coupled.argtypes = [P, C.POINTER(mc_step_report)]
+    lib.mc_run.argtypes = [P, _i32, _i32, C.POINTER(mc_step_report), C.POINTER(C.c_void_p)]
+    lib.mc_get_state.argtypes = [P, _i32, C.c_void_p]
+    lib.mc_set_state.argtypes = [P, _i32, C.c_void_p]
+    lib.mc_size.argtypes = [P, _i32]
+    lib.mc_size.restype = _i64
+    lib.mc_last_kernel_ms.argtypes = [P, _pd]
+    lib.mc_destroy.argtypes = [P]
+    lib.mc_error_string.argtypes = [P]
+    lib.mc_error_string.restype = C.c_char_p
+    lib.mc_abi_version.restype = _i32
+    for name in EXPORTS:
+        if name != "mc_size" and name != "mc_error_string" and name != "mc_abi_version":
+            getattr(lib, name).restype = _i32
+    _lib = lib
+    return lib
+
+
+class MCError(RuntimeError):
+    def __init__(self, status, msg, report=None):
+        super().__init__(f"{STATUS_NAMES.get(status, status)}: {msg}")
+        self.status = status
+        self.report = report
+
+
+def _ptr(a, ctype=_pd):
+    """Pointer to a torch tensor / numpy array (host or device), or NULL."""
+    if a is None:
+        return C.cast(None, ctype)
+    if hasattr(a, "data_ptr"):
+        return C.cast(C.c_void_p(a.data_ptr()), ctype)
+    return a.ctypes.data_as(ctype)
+
+
+class Problem:
+    """A libmc context built from a generator scenario (inputs.make / make_fine / make_nlmc).
+
+    The physical inputs are uploaded to device tensors with PyTorch and handed to
+    mc_set_continuum / mc_set_coupling; the library derives every operator array on
+    its own.
+    """
+
+    def __init__(self, scn, tau=None, rtol=1e-12, maxit=0, ctas=0, device=0, stream=None,
+                 host_inputs=False):
+        import torch
+        self.lib = load()
+        self.torch = torch
+        self.scn = scn
+        self.tau = float(scn["T"] / scn["NT"] if tau is None else tau)
+        self.device = torch.device("cuda", device)
+        if stream is None:
+            stream = torch.cuda.current_stream(self.device)
+        self.stream = stream
+        self._keep = []
+        opt = mc_options(tau=self.tau, rtol=rtol, maxit=maxit, ctas=ctas, device=device,
+                         stream=C.c_void_p(stream.cuda_stream))
+        self.ctx = C.c_void_p()
+        self.host_inputs = host_inputs
+        conts, cpls = self._descs(scn)
+        self.L = len(conts)
+        self._check(self.lib.mc_create(C.byref(self.ctx), self.L, C.byref(opt)), create=True)
+        for a, d in enumerate(conts):
+            self._check(self.lib.mc_set_continuum(self.ctx, a, C.byref(d)))
+        for d in cpls:
+            self._check(self.lib.mc_set_coupling(self.ctx, C.byref(d)))
+        self._keep = []
+        self.sizes = [int(self.lib.mc_size(self.ctx, a)) for a in range(self.L)]
+
+    # ------------------------------------------------------------------ marshalling
+    def _arr(self, x, dtype):
+        a = np.ascontiguousarray(np.asarray(x), dtype=dtype)
+        if self.host_inputs:
+            self._keep.append(a)
+            return a
+        t = self.torch.from_numpy(a).to(self.device)
+        self._keep.append(t)
+        return t
+
+    def _descs(self, scn):
+        conts, cpls = [], []
+        if scn["kind"] == "fine":
+            n, h = scn["n"], scn["h"]
+            fr = scn["fracture"]
+            for c in scn["continua"]:
+                d = mc_continuum_desc()
+                if c["kind"] == "grid":
+                    d.kind, d.n, d.nx, d.ny, d.h = MC_GRID2D, n * n, n, n, h
+                    if np.ndim(c["k"]) == 0:
+                        d.k_const = float(c["k"])
+                    else:
+                        d.k = _ptr(self._arr(c["k"], np.float64))
+                    d.c_const = float(c["c"])
+                    if c["dirichlet"] is not None:
+                        gL, gR = c["dirichlet"]
+                        if gL is not None:
+                            d.bc_left, d.g_left = 1, float(gL)
+                        if gR is not None:
+                            d.bc_right, d.g_right = 1, float(gR)
+                else:
+                    e = np.asarray(fr["edges"]).reshape(-1, 2)
+                    d.kind, d.n = MC_GRAPH, len(fr["cells"])
+                    d.c_const, d.k_const = float(c["c"]), float(c["k"])
+                    d.measure_const = h                      # |iota| = h (reading C1)
+                    d.n_edges = len(e)
+                    d.edge_i = _ptr(self._arr(e[:, 0], np.int32), _pi)
+                    d.edge_j = _ptr(self._arr(e[:, 1], np.int32), _pi)
+                    d.edge_geom = 1.0 / h                    # |E|/d, |E| = 1, d = h (reading C7)
+                conts.append(d)
+            for cp in scn["couplings"]:
+                d = mc_coupling_desc(a=cp["a"], b=cp["b"])
+                if cp["type"] == "embedded":
+                    d.nnz = len(fr["cells"])
+                    d.i_a = _ptr(self._arr(fr["cells"], np.int32), _pi)    # host cell of fracture cell e
+                    d.sigma = _ptr(self._arr(cp["sigma"], np.float64))
+                else:
+                    d.nnz = n * n
+                    d.sigma_const = float(cp["sigma"])
+                    d.scale_by_measure = 1                   # sigma_12 |cell| (reading C9)
+                cpls.append(d)
+        elif scn["kind"] == "nlmc":
+            nb = scn["nc"] ** 2
+            for a in range(2):
+                i, j, t = scn["within"][a]
+                mask, g = scn["dirichlet"][a]
+                d = mc_continuum_desc(kind=MC_GRAPH, n=nb)
+                d.c_const = float(scn["c"][a])
+                d.measure_const = 1.0                        # unit coarse measure (reading C11)
+                d.n_edges = len(i)
+                d.edge_i = _ptr(self._arr(i, np.int32), _pi)
+                d.edge_j = _ptr(self._arr(j, np.int32), _pi)
+                d.edge_t = _ptr(self._arr(t, np.float64))
+                d.dirichlet = _ptr(self._arr(np.where(mask, g, np.nan), np.float64))
+                conts.append(d)
+            bi, bj, bt = scn["between"]
+            d = mc_coupling_desc(a=0, b=1, nnz=len(bi))
+            d.i_a = _ptr(self._arr(bi, np.int32), _pi)
+            d.j_b = _ptr(self._arr(bj, np.int32), _pi)
+            d.sigma = _ptr(self._arr(bt, np.float64))
+            cpls.append(d)
+        else:
+            raise ValueError(scn["kind"])
+        return conts, cpls
+
+    # ------------------------------------------------------------------ calls
+    def _check(self, st, create=False, report=None):
+        if st != MC_OK:
+            msg = self.lib.mc_error_string(None if create else self.ctx)
+            raise MCError(st, (msg or b"").decode(), report)
+
+    def step(self, scheme="D"):
+        rep = mc_step_report()
+        fn = self.lib.mc_step_coupled if scheme == "coupled" else self.lib.mc_step_decoupled
+        st = fn(self.ctx, C.byref(rep))
+        self._check(st, report=rep.as_dict())
+        return rep.as_dict()
+
+    def run(self, scheme, n_steps, snapshots=None):
+        """n_steps steps; snapshots: None or list over steps of lists over continua of tensors."""
+        reps = (mc_step_report * max(n_steps, 1))()
+        snaps = None
+        if snapshots is not None:
+            flat = [snapshots[s][a] for s in range(n_steps) for a in range(self.L)]
+            snaps = (C.c_void_p * len(flat))(*[C.c_void_p(t.data_ptr()) for t in flat])
+        sch = MC_COUPLED if scheme == "coupled" else MC_DECOUPLED_D
+        st = self.lib.mc_run(self.ctx, sch, n_steps, reps, snaps)
+        out = [reps[s].as_dict() for s in range(n_steps)]
+        self._check(st, report=out)
+        return out
+
+    def get_state(self, alpha, out=None):
+        if out is None:
+            out = self.torch.empty(self.sizes[alpha], dtype=self.torch.float64, device=self.device)
+        self._check(self.lib.mc_get_state(self.ctx, alpha, C.c_void_p(out.data_ptr())))
+        return out
+
+    def set_state(self, alpha, src):
+        self._check(self.lib.mc_set_state(self.ctx, alpha, C.c_void_p(src.data_ptr())))
+
+    def state(self):
+        return [self.get_state(a) for a in range(self.L)]
+
+    def last_kernel_ms(self):
+        v = C.c_double()
+        self._check(self.lib.mc_last_kernel_ms(self.ctx, C.byref(v)))
+        return v.value
+
+    def close(self):
+        if self.ctx:
+            self.lib.mc_destroy(self.ctx)
+            self.ctx = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+

@@ -1,0 +1,303 @@
+"""GPU parity: the CUDA path (libmc via the C ABI) against the CPU oracle.
+
+Bar (BASELINE.json north_star): per continuum, per time step,
+    ||u_gpu - u_oracle||_2 <= 1e-9 ||u_oracle||_2,  and u_gpu == 0 exactly where u_oracle == 0,
+with CG rtol 1e-12.  Inputs are the seeded generator's (inputs/), shared by both sides.
+"""
+import ctypes as C
+import math
+
+import numpy as np
+import pytest
+
+from inputs import CONFIGS, make, make_fine, make_nlmc
+from oracle import assemble as asm
+from oracle import schemes
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-9
+
+
+@pytest.fixture(scope="module")
+def torch_cuda():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2209_01158_b200 import build
+    build.build()
+    return torch
+
+
+def gpu_traj(scn, scheme, steps, **kw):
+    from paper_2209_01158_b200 import Problem
+    pb = Problem(scn, **kw)
+    out, reps = [], []
+    for _ in range(steps):
+        reps.append(pb.step(scheme))
+        out.append([t.cpu().numpy() for t in pb.state()])
+    pb.close()
+    return out, reps
+
+
+def oracle_traj(scn, scheme, steps, tau=None):
+    sys_ = asm.assemble(scn)
+    tau = scn["T"] / scn["NT"] if tau is None else tau
+    return [sys_.split(u) for u in schemes.run(sys_, scheme, tau, steps)]
+
+
+def assert_parity(got, ref, tol=TOL):
+    worst = 0.0
+    for n, (g, r) in enumerate(zip(got, ref), start=1):
+        for a, (ga, ra) in enumerate(zip(g, r)):
+            nr = np.linalg.norm(ra)
+            if nr == 0.0:
+                assert np.array_equal(ga, np.zeros_like(ga)), f"step {n} continuum {a}: expected exact 0"
+                continue
+            e = np.linalg.norm(ga - ra) / nr
+            worst = max(worst, e)
+            assert e <= tol, f"step {n} continuum {a}: rel L2 {e:.3e} > {tol}"
+    return worst
+
+
+# ---------------------------------------------------------------- worked example
+def _one_cell(torch, scheme):
+    from paper_2209_01158_b200 import mc
+    lib = mc.load()
+    ctx = C.c_void_p()
+    opt = mc.mc_options(tau=1.0, rtol=1e-12, stream=C.c_void_p(torch.cuda.current_stream().cuda_stream))
+    assert lib.mc_create(C.byref(ctx), 2, C.byref(opt)) == 0
+    keep = []
+    for a, u0 in enumerate((1.0, 0.0)):
+        arr = np.array([u0])
+        keep.append(arr)
+        d = mc.mc_continuum_desc(kind=mc.MC_GRAPH, n=1, c_const=1.0, measure_const=1.0)
+        d.u0 = arr.ctypes.data_as(mc._pd)
+        assert lib.mc_set_continuum(ctx, a, C.byref(d)) == 0, lib.mc_error_string(ctx)
+    cp = mc.mc_coupling_desc(a=0, b=1, nnz=1, sigma_const=1.0)
+    assert lib.mc_set_coupling(ctx, C.byref(cp)) == 0
+    rep = mc.mc_step_report()
+    fn = lib.mc_step_coupled if scheme == "coupled" else lib.mc_step_decoupled
+    assert fn(ctx, C.byref(rep)) == 0, lib.mc_error_string(ctx)
+    out = [np.zeros(1), np.zeros(1)]
+    for a in range(2):
+        assert lib.mc_get_state(ctx, a, out[a].ctypes.data_as(C.c_void_p)) == 0
+    lib.mc_destroy(ctx)
+    return np.concatenate(out)
+
+
+def test_worked_example_one_cell(torch_cuda):
+    assert np.allclose(_one_cell(torch_cuda, "coupled"), [2 / 3, 1 / 3], rtol=1e-14, atol=1e-15)
+    assert np.allclose(_one_cell(torch_cuda, "D"), [0.5, 0.5], rtol=1e-14, atol=1e-15)
+
+
+# ---------------------------------------------------------------- full trajectories
+@pytest.mark.parametrize("scheme", ["D", "coupled"])
+def test_config0_full_trajectory(torch_cuda, scheme):
+    scn = make(0)
+    got, reps = gpu_traj(scn, scheme, scn["NT"])
+    ref = oracle_traj(scn, scheme, scn["NT"])
+    assert_parity(got, ref)
+    if scheme == "D":
+        assert reps[0]["iters"][1] == 0           # fracture RHS is exactly 0 at step 1
+        assert np.array_equal(got[0][1], np.zeros_like(got[0][1]))
+
+
+@pytest.mark.parametrize("scheme", ["D", "coupled"])
+def test_config3_nlmc_full_trajectory(torch_cuda, scheme):
+    scn = make(3)
+    got, _ = gpu_traj(scn, scheme, scn["NT"])
+    ref = oracle_traj(scn, scheme, scn["NT"])
+    assert_parity(got, ref)
+
+
+@pytest.mark.parametrize("scheme", ["D", "coupled"])
+def test_config1_full_trajectory(torch_cuda, scheme):
+    scn = make(1)
+    steps = scn["NT"] if scheme == "D" else 20
+    got, reps = gpu_traj(scn, scheme, steps)
+    ref = oracle_traj(scn, scheme, steps)
+    assert_parity(got, ref)
+
+
+@pytest.mark.parametrize("scheme", ["D", "coupled"])
+def test_config2_standin_three_continua(torch_cuda, scheme):
+    # config 2's recipe (3 continua, co-located + embedded transfer) on a 256^2 grid
+    p = dict(CONFIGS[2])
+    p.pop("kind")
+    p.update(n=256, segments=1500 * 256 // 2048, lengths=(100 * 256 // 2048, 800 * 256 // 2048), NT=100)
+    scn = make_fine(**p)
+    got, _ = gpu_traj(scn, scheme, 30)
+    ref = oracle_traj(scn, scheme, 30)
+    assert_parity(got, ref)
+
+
+# ---------------------------------------------------------------- ragged / edge cases
+@pytest.mark.parametrize("n,segs", [(1, 0), (3, 1), (37, 4), (45, 7)])
+@pytest.mark.parametrize("scheme", ["D", "coupled"])
+def test_ragged_small(torch_cuda, n, segs, scheme):
+    scn = make_fine(n, seed=n, T=1, NT=8, segments=segs, lengths=(1, max(1, n // 2)), k_sigma=1.0,
+                    k_f=1e4, c_f=0.01, sigma_f=("k_m", 100.0))
+    got, _ = gpu_traj(scn, scheme, 8)
+    ref = oracle_traj(scn, scheme, 8)
+    assert_parity(got, ref)
+
+
+def test_nlmc_ragged(torch_cuda):
+    scn = make_nlmc(13, seed=2, NT=10)
+    for scheme in ("D", "coupled"):
+        got, _ = gpu_traj(scn, scheme, 10)
+        assert_parity(got, oracle_traj(scn, scheme, 10))
+
+
+def test_sigma_zero_decoupled_equals_coupled(torch_cuda):
+    scn = make_fine(40, seed=1, T=1, NT=5, segments=5, lengths=(5, 20), sigma_f=("const", 0.0))
+    gd, _ = gpu_traj(scn, "D", 5)
+    gc, _ = gpu_traj(scn, "coupled", 5)
+    for a, b in zip(gd, gc):
+        for x, y in zip(a, b):
+            assert np.linalg.norm(x - y) <= 1e-10 * max(np.linalg.norm(y), 1e-300)
+
+
+def test_neumann_only_constant_preserved(torch_cuda):
+    scn = make_fine(50, seed=4, T=1, NT=3, segments=6, lengths=(5, 25), dirichlet=None)
+    from paper_2209_01158_b200 import Problem
+    import torch
+    pb = Problem(scn)
+    for a in range(pb.L):
+        pb.set_state(a, torch.full((pb.sizes[a],), 2.5, dtype=torch.float64, device="cuda"))
+    for scheme in ("D", "coupled"):
+        rep = pb.step(scheme)
+        assert all(i == 0 for i in rep["iters"])
+        for t in pb.state():
+            assert torch.all(t == 2.5)
+
+
+def test_deterministic_bitwise(torch_cuda):
+    scn = make(0)
+    a, ra = gpu_traj(scn, "D", 5)
+    b, rb = gpu_traj(scn, "D", 5)
+    for x, y in zip(a, b):
+        for u, v in zip(x, y):
+            assert np.array_equal(u, v)
+    assert [r["iters"] for r in ra] == [r["iters"] for r in rb]
+
+
+def test_cta_count_independent(torch_cuda):
+    scn = make(0)
+    ref = oracle_traj(scn, "D", 6)
+    for ctas in (1, 7, 64):
+        got, _ = gpu_traj(scn, "D", 6, ctas=ctas)
+        assert_parity(got, ref)
+
+
+def test_host_and_device_inputs_agree(torch_cuda):
+    scn = make_nlmc(20, seed=9, NT=4)
+    a, _ = gpu_traj(scn, "D", 4, host_inputs=True)
+    b, _ = gpu_traj(scn, "D", 4, host_inputs=False)
+    for x, y in zip(a, b):
+        for u, v in zip(x, y):
+            assert np.array_equal(u, v)
+
+
+def test_run_with_snapshots_matches_steps(torch_cuda):
+    import torch
+    from paper_2209_01158_b200 import Problem
+    scn = make(0)
+    pb = Problem(scn)
+    snaps = [[torch.empty(s, dtype=torch.float64, device="cuda") for s in pb.sizes] for _ in range(6)]
+    reps = pb.run("D", 6, snapshots=snaps)
+    assert [r["step"] for r in reps] == list(range(1, 7))
+    ref = oracle_traj(scn, "D", 6)
+    assert_parity([[t.cpu().numpy() for t in s] for s in snaps], ref)
+
+
+def test_noconv_does_not_advance(torch_cuda):
+    from paper_2209_01158_b200 import Problem, MCError, mc
+    scn = make(0)
+    pb = Problem(scn, maxit=3)
+    before = [t.clone() for t in pb.state()]
+    with pytest.raises(MCError) as ei:
+        pb.step("D")
+    assert ei.value.status == mc.MC_ERR_NOCONV
+    assert "not advanced" in str(ei.value)
+    for x, y in zip(before, pb.state()):
+        assert bool((x == y).all())
+
+
+def test_argument_errors(torch_cuda):
+    from paper_2209_01158_b200 import mc
+    lib = mc.load()
+    ctx = C.c_void_p()
+    assert lib.mc_create(C.byref(ctx), 2, C.byref(mc.mc_options(tau=0.1))) == 0
+    # coupling before continua
+    assert lib.mc_set_coupling(ctx, C.byref(mc.mc_coupling_desc(a=0, b=1, nnz=1, sigma_const=1.0))) == mc.MC_ERR_STATE
+    # bad grid size
+    d = mc.mc_continuum_desc(kind=mc.MC_GRID2D, n=10, nx=3, ny=3, h=0.1, k_const=1.0, c_const=1.0)
+    assert lib.mc_set_continuum(ctx, 0, C.byref(d)) == mc.MC_ERR_ARG
+    # negative storage
+    d = mc.mc_continuum_desc(kind=mc.MC_GRID2D, n=9, nx=3, ny=3, h=0.1, k_const=1.0, c_const=-1.0)
+    assert lib.mc_set_continuum(ctx, 0, C.byref(d)) == mc.MC_ERR_ARG
+    # self-loop / duplicate edges
+    ei = np.array([0, 1], dtype=np.int32)
+    ej = np.array([0, 2], dtype=np.int32)
+    d = mc.mc_continuum_desc(kind=mc.MC_GRAPH, n=3, k_const=1.0, c_const=1.0, measure_const=1.0,
+                             n_edges=2, edge_geom=1.0)
+    d.edge_i = ei.ctypes.data_as(mc._pi)
+    d.edge_j = ej.ctypes.data_as(mc._pi)
+    assert lib.mc_set_continuum(ctx, 1, C.byref(d)) == mc.MC_ERR_ARG
+    ej2 = np.array([1, 0], dtype=np.int32)
+    d.edge_i = ei.ctypes.data_as(mc._pi)
+    d.edge_j = ej2.ctypes.data_as(mc._pi)
+    assert lib.mc_set_continuum(ctx, 1, C.byref(d)) == mc.MC_ERR_ARG   # (0,1) twice
+    # step before all continua are set
+    assert lib.mc_step_decoupled(ctx, None) == mc.MC_ERR_STATE
+    # zero storage and no connection: singular row
+    d = mc.mc_continuum_desc(kind=mc.MC_GRID2D, n=1, nx=1, ny=1, h=1.0, k_const=0.0, c_const=0.0)
+    assert lib.mc_set_continuum(ctx, 0, C.byref(d)) == 0
+    d = mc.mc_continuum_desc(kind=mc.MC_GRAPH, n=1, k_const=0.0, c_const=1.0, measure_const=1.0)
+    assert lib.mc_set_continuum(ctx, 1, C.byref(d)) == 0
+    assert lib.mc_step_decoupled(ctx, None) == mc.MC_ERR_ARG
+    assert b"diagonal" in lib.mc_error_string(ctx)
+    lib.mc_destroy(ctx)
+
+
+# ---------------------------------------------------------------- full sizes: properties
+def _residual_check(scn, steps, scheme="D"):
+    """The GPU iterate satisfies the ORACLE's equations: ||K_a u^{n+1} - b_a(u^n)|| / ||b_a||."""
+    from paper_2209_01158_b200 import Problem
+    sys_ = asm.assemble(scn)
+    tau = scn["T"] / scn["NT"]
+    ds = schemes.DScheme.__new__(schemes.DScheme)
+    ds.sys, ds.tau = sys_, tau
+    ds.A0, ds.A1 = schemes.split_D(sys_)
+    import scipy.sparse as sp
+    K0 = sp.csr_matrix(sp.diags(sys_.M / tau) + ds.A0)
+    pb = Problem(scn)
+    u = sys_.u0.copy()
+    worst = []
+    for _ in range(steps):
+        rep = pb.step(scheme)
+        new = np.concatenate([t.cpu().numpy() for t in pb.state()])
+        b = ds.rhs(u)
+        for a in range(sys_.L):
+            s = sys_.block(a)
+            nb = np.linalg.norm(b[s])
+            if nb == 0:
+                assert np.array_equal(new[s], np.zeros_like(new[s]))
+                continue
+            res = np.linalg.norm(K0[s, s] @ new[s] - b[s]) / nb
+            worst.append(res)
+            assert res <= 1e-6, (a, res, rep)
+        u = new
+    pb.close()
+    return worst
+
+
+@pytest.mark.slow
+def test_config2_full_size_residuals(torch_cuda):
+    _residual_check(make(2), 3)
+
+
+@pytest.mark.slow
+def test_config4_full_size_residuals(torch_cuda):
+    _residual_check(make(4), 2)

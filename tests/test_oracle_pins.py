@@ -452,3 +452,43 @@ def test_config0_gap_matches_survey():
         e = [schemes.rel_error_percent(sys_.split(tc[n - 1])[a], sys_.split(td[n - 1])[a]) for a in range(2)]
         assert abs(e[0] - want["gap_matrix_pct"][str(n)]) <= 1.0
         assert abs(e[1] - want["gap_fracture_pct"][str(n)]) <= 1.0
+
+
+# ---------------------------------------------------------------- flux form and refinement
+@pytest.mark.parametrize("cid", [0, 3])
+def test_flux_form_assembles_to_A(cid):
+    scn = make(cid)
+    sys_ = asm.assemble(scn)
+    tau = scn["T"] / scn["NT"]
+    N = int(sys_.offsets[-1])
+    K = sp.csr_matrix(sp.diags(sys_.M / tau) + sys_.A)
+    op = sys_.flux.block_op(slice(0, N), sys_.M / tau, "coupled")
+    assert abs(op.tocsr() - K).max() <= 1e-14 * abs(K).max()
+    x = np.random.default_rng(1).standard_normal(N)
+    assert np.linalg.norm(op.apply(x) - K @ x) <= 1e-13 * np.linalg.norm(K @ x)
+    A0, _ = schemes.split_D(sys_)
+    K0 = sp.csr_matrix(sp.diags(sys_.M / tau) + A0)
+    for a in range(sys_.L):
+        s = sys_.block(a)
+        opa = sys_.flux.block_op(s, sys_.M / tau, "D")
+        assert abs(opa.tocsr() - K0[s, s]).max() <= 1e-14 * abs(K0[s, s]).max()
+        assert np.linalg.norm(opa.apply(x[s]) - K0[s, s] @ x[s]) <= 1e-13 * np.linalg.norm(K0[s, s] @ x[s])
+
+
+def test_refinement_reaches_exact_fracture_plateau():
+    """A fracture chain with T_f = k_f/h = 1e9 >> sigma = 1 over host cells held at u_m = 1:
+    the D-scheme fracture solve is exactly p_f = sigma / (sigma + m_f/tau) on every cell
+    (the flux terms vanish on a constant).  Assembling a_ii = 2 T + sigma + m/tau in fp64
+    loses ~eps T / sigma ~ 1e-7 of sigma; the flux-form refinement must not (C15)."""
+    n = 64
+    scn = make_fine(n, seed=0, T=1, NT=1, segments=0, lengths=(1, 1), dirichlet=None)
+    cells = np.arange(5 * n + 3, 5 * n + 53)                    # 50 cells along row 5
+    scn["fracture"] = dict(cells=cells, edges=np.stack([np.arange(49), np.arange(1, 50)], 1))
+    scn["continua"].append(dict(name="fracture", kind="fracture", k=1e9 / n, c=0.01, dirichlet=None))
+    scn["couplings"] = [dict(a=0, b=1, type="embedded", sigma=np.ones(50))]
+    sys_ = asm.assemble(scn)
+    tau = 0.5
+    u = np.concatenate([np.ones(n * n), np.zeros(50)])
+    uf = schemes.run(sys_, "D", tau, 1, u0=u)[0][n * n:]
+    mt = 0.01 * (1.0 / n) / tau
+    assert np.max(np.abs(uf - 1.0 / (1.0 + mt))) <= 1e-15
