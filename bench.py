@@ -1,0 +1,316 @@
+#!/usr/bin/env python
+"""Benchmark: fine-grid DOF-steps/s of the decoupled D-scheme (fp64) on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C] [--scheme D|coupled]
+                    [--impl reference]
+
+One "step" is one time layer of the D-scheme over the whole
+workload: the lagged right-hand side of every continuum, one Jacobi-PCG solve per
+continuum to rtol 1e-12 and the commit — one launch of libmc's persistent step
+kernel.  Default workload: BASELINE.json configs[1] (1024^2 matrix + 72,738
+fracture cells, log-normal k).  The inputs are seeded synthetic
+(inputs/); nothing here reads /root/reference.
+
+Timing: W untimed warm-up steps, then exactly K steps, each bracketed by CUDA
+events on the stream libmc launches on; L2 is flushed (256 MiB memset) between
+timed steps, outside the events.  Multi-GPU: one process per GPU (torchrun), each
+rank an independent replica (replicas only), max-over-ranks time.
+
+The CPU oracle (oracle/) runs here only as the `cpu_baseline` leg (rank 0, N=1) and
+as `--impl reference`; it is never on the product path.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+FALLBACK_HBM_GBS = 6650.0
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", type=int, default=1)
+    ap.add_argument("--scheme", default="D", choices=["D", "coupled"])
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)"
+
+
+def workload_name(cid, scheme):
+    return {0: "config0: 64^2 2C fine FV", 1: "config1: 1024^2 2C fine FV, lognormal k",
+            2: "config2: 2048^2 3C fine FV", 3: "config3: NLMC 2x256^2 coarse",
+            4: "config4: 8192^2 2C fine FV, lognormal k"}[cid] + f", {scheme}-scheme"
+
+
+# ------------------------------------------------------------------ algorithmic bytes
+def step_bytes(pb, rep, scheme):
+    """Algorithmic HBM bytes of one step kernel: per CG iteration every
+    row reads x, r, q, p, D^-1 and its shift, writes x, r, p, q once; grid rows read
+    Tx, Ty; graph rows read their row pointer and column indices (values when not
+    uniform).  Init pass: ~76 B/row + 16 B per transfer entry.  Neighbour gathers are
+    cache hits and not counted."""
+    sizes, kinds, nnz_off = pb.byte_model
+    total = 0.0
+    iters = rep["iters"]
+    for a, n in enumerate(sizes):
+        per = 96.0 if kinds[a] == "grid" else 84.0 + nnz_off[a]
+        it = iters[0] if scheme == "coupled" else iters[a]
+        total += it * per * n + 76.0 * n
+    return total
+
+
+def model_for(scn):
+    sizes, kinds, off = [], [], []
+    if scn["kind"] == "fine":
+        n = scn["n"]
+        for c in scn["continua"]:
+            if c["kind"] == "grid":
+                sizes.append(n * n)
+                kinds.append("grid")
+                off.append(0.0)
+            else:
+                nf = len(scn["fracture"]["cells"])
+                sizes.append(nf)
+                kinds.append("graph")
+                off.append(4.0 * 2 * len(scn["fracture"]["edges"]) / nf)          # col int32
+    else:
+        nb = scn["nc"] ** 2
+        for a in range(2):
+            sizes.append(nb)
+            kinds.append("graph")
+            off.append(12.0 * 2 * len(scn["within"][a][0]) / nb)                  # col + val
+    return sizes, kinds, off
+
+
+# ------------------------------------------------------------------ clocks
+class Clocks:
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.p = None
+
+    def start(self):
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                       "--format=csv,noheader,nounits", "-lms", "200"],
+                                      stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return None
+        self.p.terminate()
+        out, _ = self.p.communicate(timeout=10)
+        sm, mx, reasons = [], 0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in out.strip().splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 7:
+                continue
+            try:
+                sm.append(float(f[0]))
+                mx = max(mx, float(f[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        if not sm:
+            return None
+        sm.sort()
+        return {"sm_mhz": sm[len(sm) // 2], "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ------------------------------------------------------------------ distributed
+def dist_init(n):
+    if n <= 1 or "RANK" not in os.environ:
+        return 0, 1, 0
+    import torch.distributed as dist
+    import torch
+    rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
+    local = int(os.environ.get("LOCAL_RANK", rank))
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl", rank=rank, world_size=world, device_id=torch.device("cuda", local))
+    return rank, world, local
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def max_over_ranks(x, world):
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+# ------------------------------------------------------------------ oracle legs (CPU)
+def oracle_sample(scn, scheme, steps, budget_s=30.0):
+    """Time the CPU oracle (as it stands) on `steps` steps of the workload; setup
+    (assembly + SuperLU factorisation) excluded and reported separately."""
+    os.environ.setdefault("OMP_NUM_THREADS", "1")
+    from oracle import assemble as asm, schemes
+    t0 = time.perf_counter()
+    sys_ = asm.assemble(scn)
+    st = schemes.make_stepper(sys_, "coupled" if scheme == "coupled" else "D", scn["T"] / scn["NT"])
+    setup = time.perf_counter() - t0
+    u = sys_.u0.copy()
+    done = 0
+    t1 = time.perf_counter()
+    while done < steps:
+        u = st.step(u)
+        done += 1
+        if time.perf_counter() - t1 > budget_s:
+            break
+    el = time.perf_counter() - t1
+    return sum(sys_.sizes), done, el, setup
+
+
+def run_reference(args):
+    rank, world, _ = dist_init(args.gpus)
+    if rank != 0:
+        return
+    from inputs import make
+    scn = make(args.config)
+    dof, done, el, setup = oracle_sample(scn, args.scheme, args.warmup + args.steps, budget_s=240.0)
+    value = dof * done / el
+    line = {"metric": "fine-grid DOF-steps/s (decoupled, fp64)", "value": value, "unit": "DOF-steps/s",
+            "n_gpus": args.gpus, "steps": done, "warmup": 0, "ms_per_step": 1e3 * el / done,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "impl": "reference",
+            "config": {"workload": workload_name(args.config, args.scheme), "dof": dof, "scheme": args.scheme},
+            "cpu_baseline": {"value": value, "unit": "DOF-steps/s", "cores": 1, "kind": "oracle",
+                             "sample": f"{done} full oracle steps (SuperLU back-solves + long-double "
+                                       f"flux-form refinement, 1 thread); setup {setup:.1f}s excluded"},
+            "e2e": {"value": value, "unit": "DOF-steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------ main
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+        return
+    import torch
+    rank, world, local = dist_init(args.gpus)
+    torch.cuda.set_device(local)
+    from inputs import make
+    from paper_2209_01158_b200 import Problem, build
+    build.build()
+    scn = make(args.config)
+    stream = torch.cuda.Stream()
+    torch.cuda.set_stream(stream)
+    pb = Problem(scn, device=local, stream=stream)
+    pb.byte_model = model_for(scn)
+    dof = sum(pb.sizes)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    for _ in range(args.warmup):
+        pb.step(args.scheme)
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    reps = []
+    clocks = Clocks(local)
+    barrier(world)
+    torch.cuda.synchronize()
+    clocks.start()
+    for k in range(args.steps):
+        flush.zero_()
+        ev[k][0].record(stream)
+        reps.append(pb.step(args.scheme))
+        ev[k][1].record(stream)
+    torch.cuda.synchronize()
+    barrier(world)
+    clk = clocks.stop()
+    step_ms = [a.elapsed_time(b) for a, b in ev]
+    total_ms = max_over_ranks(sum(step_ms), world)
+    value = world * dof * args.steps / (total_ms * 1e-3)
+    # roofline of the dominant (only) kernel: the step kernel, one launch per step
+    bytes_per = sum(step_bytes(pb, r, args.scheme) for r in reps) / args.steps
+    kern_ms = sum(r["ms"] for r in reps) / args.steps
+    peak, peak_src = peaks()
+    achieved = bytes_per / (kern_ms * 1e-3) / 1e9
+    # end to end through the C ABI with host buffers (pinned), copies inside the timed region
+    e2e = None
+    if not args.no_e2e:
+        host = [torch.empty(s, dtype=torch.float64, pin_memory=True) for s in pb.sizes]
+        for a in range(pb.L):
+            pb.get_state(a, out=host[a])
+        torch.cuda.synchronize()
+        barrier(world)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(args.steps):
+            for a in range(pb.L):
+                pb.set_state(a, host[a])
+            pb.step(args.scheme)
+            for a in range(pb.L):
+                pb.get_state(a, out=host[a])
+        e1.record(stream)
+        torch.cuda.synchronize()
+        e2e_ms = max_over_ranks(e0.elapsed_time(e1), world)
+        e2e = {"value": world * dof * args.steps / (e2e_ms * 1e-3), "unit": "DOF-steps/s",
+               "h2d_bytes_per_step": 8 * dof, "d2h_bytes_per_step": 8 * dof}
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        d, done, el, setup = oracle_sample(scn, args.scheme, 3 if args.config in (1, 2, 4) else 20, budget_s=25.0)
+        cpu = {"value": d * done / el, "unit": "DOF-steps/s", "cores": 1, "kind": "oracle",
+               "sample": f"config{args.config} {args.scheme}-scheme, {done} oracle steps (SuperLU back-solves "
+                         f"+ long-double flux refinement, 1 thread); assembly+factorisation {setup:.1f}s excluded"}
+    its = [r["iters"] for r in reps]
+    mean_its = [sum(x[a] for x in its) / len(its) for a in range(len(its[0]))]
+    if rank == 0:
+        line = {
+            "metric": "fine-grid DOF-steps/s (decoupled, fp64)", "value": value, "unit": "DOF-steps/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": total_ms / args.steps, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": workload_name(args.config, args.scheme), "dof": dof,
+                       "sizes": pb.sizes, "scheme": args.scheme, "rtol": 1e-12,
+                       "cg_iters_per_step": mean_its,
+                       "ms_per_solve": [sum(r["ms_solve"][a] for r in reps) / len(reps) for a in range(len(reps[0]["ms_solve"]))],
+                       "l2": "flushed between timed steps (256 MiB memset)",
+                       "parallelism": f"replicas x{world}"},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": None, "peak_source": peak_src,
+                         "kernel": "mc::step_kernel", "bytes_per_launch": bytes_per,
+                         "ms_per_launch": kern_ms},
+            "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": args.steps, "clocks": clk,
+        }
+        print(json.dumps(line), flush=True)
+    pb.close()
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

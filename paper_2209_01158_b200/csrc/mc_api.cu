@@ -32,6 +32,7 @@ struct HostCont {
   std::vector<int32_t> rowptr, col;            // graph, local columns
   std::vector<double> val;                     // graph per-entry T (empty -> uniform)
   double Tconst = 0.0;
+  int64_t col_count = 0;                       // graph: stored off-diagonal entries
   std::vector<uint8_t> fixed;                  // graph Dirichlet DOFs
   std::vector<double> gfix;
 };
@@ -75,6 +76,7 @@ struct mc_ctx {
   int32_t* rowptr[MC_MAX_CONTINUA] = {nullptr};
   int32_t* col[MC_MAX_CONTINUA] = {nullptr};
   double* val[MC_MAX_CONTINUA] = {nullptr};
+  int32_t* ecol[MC_MAX_CONTINUA] = {nullptr};
   double* partials = nullptr;
   SyncBlock* sync = nullptr;
   GroupOut* gout = nullptr;
@@ -605,6 +607,18 @@ static mc_status finalize(mc_ctx* c) {
     } else {
       std::vector<int32_t> gcol(H.col);
       for (auto& v : gcol) v += (int32_t)c->off[a];
+      H.col_count = (int64_t)H.col.size();
+      // ELL copy (width 4, k-major) when every row has <= 4 neighbours: one coalesced
+      // trip for the structure instead of rowptr -> col
+      int maxdeg = 0;
+      for (int64_t i = 0; i < H.n; ++i) maxdeg = std::max(maxdeg, H.rowptr[(size_t)i + 1] - H.rowptr[(size_t)i]);
+      if (maxdeg <= 4 && H.val.empty()) {
+        std::vector<int32_t> ell((size_t)(4 * H.n), -1);
+        for (int64_t i = 0; i < H.n; ++i)
+          for (int32_t e = H.rowptr[(size_t)i], k = 0; e < H.rowptr[(size_t)i + 1]; ++e, ++k)
+            ell[(size_t)(k * H.n + i)] = H.col[(size_t)e] + (int32_t)c->off[a];
+        UP(c->ecol[a], ell);
+      }
       UP(c->rowptr[a], H.rowptr);
       UP(c->col[a], gcol);
       if (!H.val.empty()) UP(c->val[a], H.val);
@@ -650,26 +664,32 @@ static mc_status finalize(mc_ctx* c) {
 }
 
 // ====================================================================== work plan
+// Work items of continuum a for `warps` warps: about one item per warp, equal sizes.
 static void add_items(const mc_ctx* c, int a, int warps, std::vector<Item>& items) {
   const HostCont& H = c->hc[a];
   warps = std::max(warps, 1);
   if (H.kind == KIND_GRID) {
-    const int strips = (H.nx + 31) / 32;
-    const int segs = std::max(1, (warps + strips - 1) / strips);
-    const int hgt = std::max(1, (H.ny + segs - 1) / segs);
-    for (int s = 0; s < strips; ++s)
-      for (int y0 = 0; y0 < H.ny; y0 += hgt) {
+    const int w = (H.nx % 2 == 0) ? 64 : 32;       // 2 columns per lane when rows stay 16-B aligned
+    const int strips = (H.nx + w - 1) / w;
+    // distribute `warps` segments over the strips (+-1), heights as equal as possible
+    const int base = std::max(1, warps / strips), extra = (warps >= strips) ? warps % strips : 0;
+    for (int s = 0; s < strips; ++s) {
+      const int segs = std::min(H.ny, base + (s < extra ? 1 : 0));
+      for (int k = 0; k < segs; ++k) {
         Item it{};
         it.cont = a;
         it.kind = ITEM_GRID;
-        it.a = s * 32;
-        it.b = y0;
-        it.c = std::min(H.ny, y0 + hgt);
-        items.push_back(it);
+        it.a = s * w;
+        it.b = (int)((int64_t)H.ny * k / segs);
+        it.c = (int)((int64_t)H.ny * (k + 1) / segs);
+        it.w = w;
+        if (it.c > it.b) items.push_back(it);
       }
+    }
   } else {
     int64_t chunk = (H.n + warps - 1) / warps;
-    chunk = std::max<int64_t>(32, (chunk + 31) / 32 * 32);
+    const int64_t q = (H.col_count > 8 * H.n) ? 4 : 32;   // rows per warp-step (LPR 8 or 1)
+    chunk = std::max<int64_t>(q, (chunk + q - 1) / q * q);
     for (int64_t r0 = 0; r0 < H.n; r0 += chunk) {
       Item it{};
       it.cont = a;
@@ -687,7 +707,10 @@ static int64_t default_maxit(const mc_ctx* c, int64_t n) {
 }
 
 // CTAs a latency-bound solve of n rows can use with >= 2 rows per thread
-static int useful_ctas(int64_t n) { return (int)std::max<int64_t>(1, (n + 2 * kThreads - 1) / (2 * kThreads)); }
+static int useful_ctas(const HostCont& H) {
+  const int64_t lanes = (H.kind == KIND_GRAPH && H.col_count > 8 * H.n) ? 8 * H.n : H.n;
+  return (int)std::max<int64_t>(1, (lanes + 2 * kThreads - 1) / (2 * kThreads));
+}
 
 static Plan make_plan(const mc_ctx* c, int scheme) {
   Plan P;
@@ -720,7 +743,7 @@ static Plan make_plan(const mc_ctx* c, int scheme) {
     if (c->last_iters[a] <= 0) hist = false;
   }
   int ctas[MC_MAX_CONTINUA] = {0};
-  if (all_large || !hist || L == 1) {
+  if (all_large || !hist || L == 1 || T < 4 * L) {
     // sequential phases, every solve on all CTAs (bandwidth-bound, or no iteration history)
     P.nphases = L;
     for (int a = 0; a < L; ++a) {
@@ -737,20 +760,36 @@ static Plan make_plan(const mc_ctx* c, int scheme) {
     for (int a = 0; a < L; ++a) {
       w[a] = (double)c->hc[a].n * (double)c->last_iters[a];
       wsum += w[a];
-      ctas[a] = std::min(useful_ctas(c->hc[a].n), std::max(1, T / (2 * L)));
+      ctas[a] = std::min(useful_ctas(c->hc[a]), std::max(1, T / (2 * L)));
       used += ctas[a];
     }
-    int rest = T - used;
-    int given = 0;
-    for (int a = 0; a < L; ++a) {
-      const int add = (int)std::floor(rest * (w[a] / wsum));
-      ctas[a] += add;
-      given += add;
+    int rest = std::max(0, T - used);
+    // distribute by work, never beyond what a solve can use (latency-bound solves pay
+    // for every extra CTA in their per-iteration barrier)
+    for (int round = 0; round < 4 && rest > 0; ++round) {
+      double wl = 0.0;
+      for (int a = 0; a < L; ++a)
+        if (ctas[a] < useful_ctas(c->hc[a])) wl += w[a];
+      if (wl <= 0.0) break;
+      int given = 0;
+      for (int a = 0; a < L; ++a) {
+        if (ctas[a] >= useful_ctas(c->hc[a])) continue;
+        int add = (int)std::floor(rest * (w[a] / wl));
+        add = std::min(add, useful_ctas(c->hc[a]) - ctas[a]);
+        ctas[a] += add;
+        given += add;
+      }
+      if (given == 0) {
+        int amax = -1;
+        for (int a = 0; a < L; ++a)
+          if (ctas[a] < useful_ctas(c->hc[a]) && (amax < 0 || w[a] > w[amax])) amax = a;
+        if (amax < 0) break;
+        const int add = std::min(rest, useful_ctas(c->hc[amax]) - ctas[amax]);
+        ctas[amax] += add;
+        given = add;
+      }
+      rest -= given;
     }
-    int amax = 0;
-    for (int a = 1; a < L; ++a)
-      if (w[a] > w[amax]) amax = a;
-    ctas[amax] += rest - given;
     int b = 0;
     for (int a = 0; a < L; ++a) {
       P.grp[a].phase = 0;
@@ -817,6 +856,10 @@ static mc_status enqueue_step(mc_ctx* c, int scheme) {
     C.col = c->col[a];
     C.val = c->val[a];
     C.Tconst = H.Tconst;
+    C.ecol = c->ecol[a];
+    C.ell = c->ecol[a] ? 4 : 0;
+    C.lpr = 1;
+    if (H.kind == KIND_GRAPH && H.n > 0 && H.col_count > 8 * H.n) C.lpr = 8;   // > 8 neighbours per row
   }
   for (int g = 0; g < cp.ngroups; ++g) P.grp[g] = cp.grp[g];
   P.L = c->L;

@@ -9,9 +9,10 @@ namespace mc {
 
 constexpr int kThreads = 256;          // threads per CTA of the step kernel
 constexpr int kWarps = kThreads / 32;
-constexpr int kMinBlocks = 4;          // __launch_bounds__ residency target (4 x 256 per SM)
+constexpr int kMinBlocks = 3;          // __launch_bounds__ residency target (3 x 256 per SM, 85 regs)
 constexpr int kNPart = 5;              // reduction slots per barrier (pq, rr, rz, rq, qq)
 constexpr int kPadDofs = 32;           // continuum offsets padded to 32 doubles (256 B)
+constexpr int kCtrStride = 32;         // barrier counters 256 B apart (own L2 line / slice)
 
 enum ContKind : int32_t { KIND_GRID = 0, KIND_GRAPH = 1 };
 enum ItemKind : int32_t { ITEM_GRID = 0, ITEM_GRAPH = 1 };
@@ -26,7 +27,10 @@ struct ContDev {
   const int32_t* rowptr;   // graph: [n+1], local
   const int32_t* col;      // graph: GLOBAL column indices
   const double* val;       // graph: per-entry T, or nullptr -> Tconst
+  const int32_t* ecol;     // graph: ELL copy of col, [ell][n] (k-major, -1 = none), or nullptr
   double Tconst;
+  int32_t lpr;             // graph: lanes per row (1 or 8)
+  int32_t ell;             // graph: ELL width (4) when ecol != nullptr
 };
 
 // a work item: a 32-column strip segment of a grid, or a row range of a graph
@@ -34,7 +38,7 @@ struct Item {
   int32_t cont;
   int32_t kind;
   int32_t a, b, c;         // grid: x0, y0, y1   graph: r0, r1, -
-  int32_t pad;
+  int32_t w;               // grid: strip width (32 scalar lanes, or 64 = 2 columns per lane)
 };
 
 // one CG solve (D-scheme: one continuum; coupled: all)
@@ -57,8 +61,9 @@ struct GroupOut {
 };
 
 struct SyncBlock {         // zeroed before every step launch
-  unsigned long long arrive[MC_MAX_CONTINUA];
+  unsigned long long arrive[MC_MAX_CONTINUA * kCtrStride];
   unsigned long long phase_arrive;
+  unsigned long long pad0[kCtrStride - 1];
   unsigned int finished;
   unsigned int pad[3];
 };

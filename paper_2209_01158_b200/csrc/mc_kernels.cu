@@ -39,6 +39,10 @@ __device__ __forceinline__ unsigned long long ld_acquire(const unsigned long lon
   return v;
 }
 
+__device__ __forceinline__ void red_release_add(unsigned long long* p, unsigned long long v) {
+  asm volatile("red.release.gpu.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
 __device__ __forceinline__ long long globaltimer() {
   long long t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -156,7 +160,139 @@ __device__ void iter_grid(const Ctx& c, const ContDev& C, int x0, int y0, int y1
   }
 }
 
+// ---------------------------------------------------------------- CG pass, grid strip, 2 columns per lane
+// (even nx): every load and store is a 16-byte double2, a warp covers 64 columns.
+__device__ __forceinline__ double2 ld2ro(const double* p) { return __ldg(reinterpret_cast<const double2*>(p)); }
+__device__ __forceinline__ double2 ld2mut(const double* p) { return __ldcg(reinterpret_cast<const double2*>(p)); }
+__device__ __forceinline__ void st2mut(double* p, double2 v) { __stcg(reinterpret_cast<double2*>(p), v); }
+
+struct Row2 {
+  double2 p, r, d;
+};
+
+__device__ __forceinline__ double2 pnew2(const Ctx& c, int64_t gi) {
+  const double2 ro = ld2mut(c.rs + gi), qo = ld2mut(c.qs + gi), po = ld2mut(c.ps + gi);
+  const double2 di = ld2ro(c.P->dinv + gi);
+  return make_double2(pnew(ro.x, qo.x, po.x, di.x, c.a, c.b), pnew(ro.y, qo.y, po.y, di.y, c.a, c.b));
+}
+
+__device__ __forceinline__ Row2 own2(const Ctx& c, int64_t gi) {
+  const double2 ro = ld2mut(c.rs + gi), qo = ld2mut(c.qs + gi), po = ld2mut(c.ps + gi);
+  const double2 di = ld2ro(c.P->dinv + gi);
+  const double2 xo = *reinterpret_cast<const double2*>(c.x + gi);
+  Row2 o;
+  o.d = di;
+  o.r = make_double2(__fma_rn(-c.a, qo.x, ro.x), __fma_rn(-c.a, qo.y, ro.y));
+  o.p = make_double2(__fma_rn(di.x, o.r.x, __dmul_rn(c.b, po.x)), __fma_rn(di.y, o.r.y, __dmul_rn(c.b, po.y)));
+  *reinterpret_cast<double2*>(c.x + gi) = make_double2(__fma_rn(c.a, po.x, xo.x), __fma_rn(c.a, po.y, xo.y));
+  st2mut(c.rd + gi, o.r);
+  st2mut(c.pd + gi, o.p);
+  return o;
+}
+
+template <bool CPL>
+__device__ void iter_grid2(const Ctx& c, const ContDev& C, int x0, int y0, int y1,
+                           double (&acc)[kNPart]) {
+  const int lane = threadIdx.x & 31;
+  const int nx = C.nx, ny = C.ny;
+  const int c0 = x0 + 2 * lane;
+  const bool valid = c0 < nx;              // nx even: c0 + 1 < nx as well
+  const int64_t off = C.off;
+  double2 pm = make_double2(0.0, 0.0), tym = make_double2(0.0, 0.0);
+  if (valid && y0 > 0) {
+    const int64_t i = (int64_t)(y0 - 1) * nx + c0;
+    pm = pnew2(c, off + i);
+    tym = ld2ro(C.Ty + i);
+  }
+  Row2 cur;
+  cur.p = cur.r = cur.d = make_double2(0.0, 0.0);
+  if (valid) cur = own2(c, off + (int64_t)y0 * nx + c0);
+  for (int y = y0; y < y1; ++y) {
+    const int64_t i = (int64_t)y * nx + c0;
+    const int64_t gi = off + i;
+    Row2 nxt;
+    nxt.p = nxt.r = nxt.d = make_double2(0.0, 0.0);
+    if (valid && y + 1 < ny) {
+      if (y + 1 < y1) nxt = own2(c, gi + nx);
+      else nxt.p = pnew2(c, gi + nx);
+    }
+    const double2 tx = valid ? ld2ro(C.Tx + i) : make_double2(0.0, 0.0);
+    double pl = __shfl_up_sync(0xffffffffu, cur.p.y, 1);
+    double pr = __shfl_down_sync(0xffffffffu, cur.p.x, 1);
+    double txl = __shfl_up_sync(0xffffffffu, tx.y, 1);
+    if (lane == 0) {
+      if (valid && c0 > 0) {
+        pl = c.pn_at(gi - 1);
+        txl = ldro(C.Tx + i - 1);
+      } else {
+        pl = 0.0;
+        txl = 0.0;
+      }
+    }
+    if (lane == 31) pr = (valid && c0 + 2 < nx) ? c.pn_at(gi + 2) : 0.0;
+    if (valid) {
+      const double2 ty = ld2ro(C.Ty + i);
+      const double2 ds = ld2ro(c.ds + gi);
+      const double2 pc = cur.p;
+      double q0 = ds.x * pc.x;
+      q0 += tx.x * (pc.x - pc.y);
+      q0 += txl * (pc.x - pl);
+      q0 += ty.x * (pc.x - nxt.p.x);
+      q0 += tym.x * (pc.x - pm.x);
+      double q1 = ds.y * pc.y;
+      q1 += tx.y * (pc.y - pr);
+      q1 += tx.x * (pc.y - pc.x);
+      q1 += ty.y * (pc.y - nxt.p.y);
+      q1 += tym.y * (pc.y - pm.y);
+      if (CPL) {
+        q0 += c.couple_q(gi, pc.x);
+        q1 += c.couple_q(gi + 1, pc.y);
+      }
+      st2mut(c.qd + gi, make_double2(q0, q1));
+      c.accum(acc, pc.x, cur.r.x, cur.d.x, q0);
+      c.accum(acc, pc.y, cur.r.y, cur.d.y, q1);
+      tym = ty;
+    }
+    pm = cur.p;
+    cur = nxt;
+  }
+}
+
+// ---------------------------------------------------------------- CG pass, graph rows, ELL
+// lane-per-row over a k-major ELL copy of the adjacency (width W, -1 = no entry): the W
+// column indices arrive in one coalesced trip, then all neighbour gathers in one more.
+template <bool CPL, int W>
+__device__ void iter_ell(const Ctx& c, const ContDev& C, int r0, int r1, double (&acc)[kNPart]) {
+  const int lane = threadIdx.x & 31;
+  const int64_t n = C.n;
+  for (int i = r0 + lane; i < r1; i += 32) {
+    const int64_t gi = C.off + i;
+    int32_t j[W];
+#pragma unroll
+    for (int k = 0; k < W; ++k) j[k] = ldro(C.ecol + k * n + i);
+    double pc, rc, dc;
+    c.own(gi, pc, rc, dc);
+    double pj[W];
+#pragma unroll
+    for (int k = 0; k < W; ++k) pj[k] = (j[k] >= 0) ? c.pn_at(j[k]) : pc;
+    double s = 0.0;
+    if (C.val) {
+#pragma unroll
+      for (int k = 0; k < W; ++k) s += (j[k] >= 0 ? ldro(C.val + k * n + i) : 0.0) * (pc - pj[k]);
+    } else {
+#pragma unroll
+      for (int k = 0; k < W; ++k) s += pc - pj[k];
+      s *= C.Tconst;
+    }
+    double qv = ldro(c.ds + gi) * pc + s;
+    if (CPL) qv += c.couple_q(gi, pc);
+    stmut(c.qd + gi, qv);
+    c.accum(acc, pc, rc, dc, qv);
+  }
+}
+
 // ---------------------------------------------------------------- CG pass, graph rows
+// lane-per-row; the edge loop gathers 4 neighbours at a time (fixed summation order)
 template <bool CPL>
 __device__ void iter_graph(const Ctx& c, const ContDev& C, int r0, int r1,
                            double (&acc)[kNPart]) {
@@ -165,18 +301,72 @@ __device__ void iter_graph(const Ctx& c, const ContDev& C, int r0, int r1,
     const int64_t gi = C.off + i;
     double pc, rc, dc;
     c.own(gi, pc, rc, dc);
-    double qv = ldro(c.ds + gi) * pc;
     const int32_t e0 = ldro(C.rowptr + i), e1 = ldro(C.rowptr + i + 1);
+    double s = 0.0;
+    int32_t e = e0;
     if (C.val) {
-      for (int32_t e = e0; e < e1; ++e) qv += ldro(C.val + e) * (pc - c.pn_at(ldro(C.col + e)));
+      for (; e + 4 <= e1; e += 4) {
+        const int32_t j0 = ldro(C.col + e), j1 = ldro(C.col + e + 1), j2 = ldro(C.col + e + 2),
+                      j3 = ldro(C.col + e + 3);
+        const double v0 = ldro(C.val + e), v1 = ldro(C.val + e + 1), v2 = ldro(C.val + e + 2),
+                     v3 = ldro(C.val + e + 3);
+        const double q0 = c.pn_at(j0), q1 = c.pn_at(j1), q2 = c.pn_at(j2), q3 = c.pn_at(j3);
+        s += v0 * (pc - q0);
+        s += v1 * (pc - q1);
+        s += v2 * (pc - q2);
+        s += v3 * (pc - q3);
+      }
+      for (; e < e1; ++e) s += ldro(C.val + e) * (pc - c.pn_at(ldro(C.col + e)));
     } else {
-      double s = 0.0;
-      for (int32_t e = e0; e < e1; ++e) s += pc - c.pn_at(ldro(C.col + e));
-      qv += C.Tconst * s;
+      for (; e + 4 <= e1; e += 4) {
+        const int32_t j0 = ldro(C.col + e), j1 = ldro(C.col + e + 1), j2 = ldro(C.col + e + 2),
+                      j3 = ldro(C.col + e + 3);
+        const double q0 = c.pn_at(j0), q1 = c.pn_at(j1), q2 = c.pn_at(j2), q3 = c.pn_at(j3);
+        s += pc - q0;
+        s += pc - q1;
+        s += pc - q2;
+        s += pc - q3;
+      }
+      for (; e < e1; ++e) s += pc - c.pn_at(ldro(C.col + e));
+      s *= C.Tconst;
     }
+    double qv = ldro(c.ds + gi) * pc + s;
     if (CPL) qv += c.couple_q(gi, pc);
     stmut(c.qd + gi, qv);
     c.accum(acc, pc, rc, dc, qv);
+  }
+}
+
+// 8 lanes per row (wide rows, e.g. the NLMC operator's ~24 neighbours): each lane sums
+// every 8th edge, then a fixed xor tree combines the 8 partial sums.
+template <bool CPL>
+__device__ void iter_graph8(const Ctx& c, const ContDev& C, int r0, int r1,
+                            double (&acc)[kNPart]) {
+  const int lane = threadIdx.x & 31, sub = lane & 7, grp = lane >> 3;
+  for (int base = r0; base < r1; base += 4) {
+    const int i = base + grp;
+    const bool ok = i < r1;
+    const int64_t gi = C.off + (ok ? i : r0);
+    double pc = 0.0, rc = 0.0, dc = 0.0;
+    if (ok && sub == 0) c.own(gi, pc, rc, dc);
+    pc = __shfl_sync(0xffffffffu, pc, lane & ~7);
+    double s = 0.0;
+    if (ok) {
+      const int32_t e0 = ldro(C.rowptr + i), e1 = ldro(C.rowptr + i + 1);
+      for (int32_t e = e0 + sub; e < e1; e += 8) {
+        const double t = C.val ? ldro(C.val + e) : C.Tconst;
+        s += t * (pc - c.pn_at(ldro(C.col + e)));
+      }
+    }
+    s += __shfl_xor_sync(0xffffffffu, s, 4);
+    s += __shfl_xor_sync(0xffffffffu, s, 2);
+    s += __shfl_xor_sync(0xffffffffu, s, 1);
+    if (ok && sub == 0) {
+      double qv = ldro(c.ds + gi) * pc + s;
+      if (CPL) qv += c.couple_q(gi, pc);
+      stmut(c.qd + gi, qv);
+      c.accum(acc, pc, rc, dc, qv);
+    }
   }
 }
 
@@ -211,8 +401,8 @@ __device__ void init_item(const StepParams& P, const Item& it, const double* uo,
   const ContDev& C = P.cont[it.cont];
   const int lane = threadIdx.x & 31;
   if (it.kind == ITEM_GRID) {
-    const int nx = C.nx, ny = C.ny, col = it.a + lane;
-    if (col >= nx) return;
+    const int nx = C.nx, ny = C.ny;
+    for (int col = it.a + lane; col < it.a + it.w && col < nx; col += 32)
     for (int y = it.b; y < it.c; ++y) {
       const int64_t i = (int64_t)y * nx + col, gi = C.off + i;
       const double u = uo[gi];
@@ -242,9 +432,8 @@ __device__ void zero_item(const StepParams& P, const Item& it, double* x) {
   const ContDev& C = P.cont[it.cont];
   const int lane = threadIdx.x & 31;
   if (it.kind == ITEM_GRID) {
-    const int col = it.a + lane;
-    if (col >= C.nx) return;
-    for (int y = it.b; y < it.c; ++y) x[C.off + (int64_t)y * C.nx + col] = 0.0;
+    for (int col = it.a + lane; col < it.a + it.w && col < C.nx; col += 32)
+      for (int y = it.b; y < it.c; ++y) x[C.off + (int64_t)y * C.nx + col] = 0.0;
   } else {
     for (int i = it.a + lane; i < it.b; i += 32) x[C.off + i] = 0.0;
   }
@@ -278,13 +467,12 @@ __device__ __forceinline__ void group_allreduce(const StepParams& P, int g, int 
       for (int i = 0; i < kWarps; ++i) s += sh[i][k];
       __stcg(part + (size_t)k * P.total_ctas + base + cl, s);
     }
-    __threadfence();
-    unsigned long long* ctr = &P.sync->arrive[g];
-    atomicAdd(ctr, 1ull);
+    // release: this CTA's r/p/q stores (ordered before by bar.sync) and its partials
+    unsigned long long* ctr = &P.sync->arrive[g * kCtrStride];
+    red_release_add(ctr, 1ull);
     const unsigned long long target = (epoch + 1ull) * (unsigned long long)G;
     while (ld_acquire(ctr) < target) {
     }
-    __threadfence();
   }
   __syncthreads();
   if (w < NP) {
@@ -326,6 +514,8 @@ __device__ void run_group(const StepParams& P, int g, int cl, double* x, const d
     zero = true;       // b = 0  =>  x = 0 after 0 iterations
     rr = 0.0;
   } else if (!(rr <= G.tol2 * bb)) {
+    Item it0{};
+    if (ib + wg < ie) it0 = P.items[ib + wg];     // most warps own exactly one item
     Ctx c;
     c.P = &P;
     c.x = x;
@@ -342,10 +532,18 @@ __device__ void run_group(const StepParams& P, int g, int cl, double* x, const d
       c.qd = P.q[s ^ 1];
       double a5[kNPart] = {0.0, 0.0, 0.0, 0.0, 0.0};
       for (int it = ib + wg; it < ie; it += W) {
-        const Item item = P.items[it];
+        const Item item = (it == ib + wg) ? it0 : P.items[it];
         const ContDev& C = P.cont[item.cont];
-        if (item.kind == ITEM_GRID) iter_grid<CPL>(c, C, item.a, item.b, item.c, a5);
-        else iter_graph<CPL>(c, C, item.a, item.b, a5);
+        if (item.kind == ITEM_GRID) {
+          if (item.w == 64) iter_grid2<CPL>(c, C, item.a, item.b, item.c, a5);
+          else iter_grid<CPL>(c, C, item.a, item.b, item.c, a5);
+        } else if (C.ecol) {
+          iter_ell<CPL, 4>(c, C, item.a, item.b, a5);
+        } else if (C.lpr == 8) {
+          iter_graph8<CPL>(c, C, item.a, item.b, a5);
+        } else {
+          iter_graph<CPL>(c, C, item.a, item.b, a5);
+        }
       }
       double t5[kNPart];
       group_allreduce<kNPart>(P, g, cl, epoch, a5, t5);
@@ -389,11 +587,9 @@ __device__ void run_group(const StepParams& P, int g, int cl, double* x, const d
 __device__ __forceinline__ void grid_barrier(const StepParams& P, unsigned long long target) {
   __syncthreads();
   if (threadIdx.x == 0) {
-    __threadfence();
-    atomicAdd(&P.sync->phase_arrive, 1ull);
+    red_release_add(&P.sync->phase_arrive, 1ull);
     while (ld_acquire(&P.sync->phase_arrive) < target) {
     }
-    __threadfence();
   }
   __syncthreads();
 }
