@@ -27,29 +27,39 @@ def _stale() -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not _stale():
+def build(force: bool = False, verbose: bool = False, defines=(), out: str | None = None) -> str:
+    """Compile csrc/*.cu for sm_100a into `out` (default: the in-tree libmc.so).
+    `defines`: extra -D macros (tuning variants, e.g. MC_STAGES=3)."""
+    lib = out or LIB
+    if not force and out is None and not _stale():
         return LIB
     objs = []
+    dflags = [f"-D{d}" for d in defines]
     for src in SOURCES:
         obj = os.path.join(CSRC, src.replace(".cu", ".o"))
-        cmd = [NVCC, *ARCH, *FLAGS, "-c", os.path.join(CSRC, src), "-o", obj]
+        cmd = [NVCC, *ARCH, *FLAGS, *dflags, "-c", os.path.join(CSRC, src), "-o", obj]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if verbose or r.returncode:
             sys.stderr.write(" ".join(cmd) + "\n" + r.stdout + r.stderr)
         if r.returncode:
             raise RuntimeError(f"nvcc failed on {src}")
         objs.append(obj)
-    cmd = [NVCC, *ARCH, "-shared", "-o", LIB + ".tmp", *objs, "-cudart", "static"]
+    cmd = [NVCC, *ARCH, "-shared", "-o", lib + ".tmp", *objs, "-cudart", "static"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode:
         sys.stderr.write(" ".join(cmd) + "\n" + r.stdout + r.stderr)
         raise RuntimeError("link failed")
-    os.replace(LIB + ".tmp", LIB)
+    os.replace(lib + ".tmp", lib)
     for o in objs:
         os.remove(o)
-    return LIB
+    return lib
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose=True))
+    # python -m paper_2209_01158_b200.build [--force] [--variant NAME DEF=1 ...]
+    if "--variant" in sys.argv:
+        i = sys.argv.index("--variant")
+        name, defs = sys.argv[i + 1], sys.argv[i + 2:]
+        print(build(force=True, verbose=True, defines=defs, out=os.path.join(PKG, f"libmc_{name}.so")))
+    else:
+        print(build(force="--force" in sys.argv, verbose=True))

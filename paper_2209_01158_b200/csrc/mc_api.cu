@@ -8,6 +8,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <numeric>
 #include <string>
@@ -33,6 +34,8 @@ struct HostCont {
   std::vector<double> val;                     // graph per-entry T (empty -> uniform)
   double Tconst = 0.0;
   int64_t col_count = 0;                       // graph: stored off-diagonal entries
+  int64_t estride = 0;                         // graph: ELL stride
+  std::vector<int32_t> perm, inv;              // graph: internal position -> caller index, inverse
   std::vector<uint8_t> fixed;                  // graph Dirichlet DOFs
   std::vector<double> gfix;
 };
@@ -77,6 +80,8 @@ struct mc_ctx {
   int32_t* col[MC_MAX_CONTINUA] = {nullptr};
   double* val[MC_MAX_CONTINUA] = {nullptr};
   int32_t* ecol[MC_MAX_CONTINUA] = {nullptr};
+  int32_t* perm[MC_MAX_CONTINUA] = {nullptr};   // graph: internal -> caller numbering
+  double* scratch = nullptr;                     // state I/O staging (max graph n)
   double* partials = nullptr;
   SyncBlock* sync = nullptr;
   GroupOut* gout = nullptr;
@@ -441,6 +446,82 @@ static mc_status set_graph(mc_ctx* c, HostCont& H, const mc_continuum_desc* d) {
   return MC_OK;
 }
 
+// Internal numbering of a graph continuum: walk the connection graph in
+// chains — start at every endpoint / junction (degree != 2) in caller order, follow
+// unvisited neighbours until the chain ends, then sweep what is left (cycles, isolated
+// cells).  Along a fracture segment consecutive cells become consecutive rows, so most
+// neighbours of a row sit in the same 64-row chunk of the CG pass.
+static void chain_order(const HostCont& H, std::vector<int32_t>& perm) {
+  const int64_t n = H.n;
+  perm.clear();
+  perm.reserve((size_t)n);
+  std::vector<uint8_t> seen((size_t)n, 0);
+  auto deg = [&](int64_t i) { return H.rowptr[(size_t)i + 1] - H.rowptr[(size_t)i]; };
+  auto walk = [&](int32_t start) {
+    int32_t cur = start;
+    while (cur >= 0 && !seen[(size_t)cur]) {
+      seen[(size_t)cur] = 1;
+      perm.push_back(cur);
+      int32_t nxt = -1;
+      for (int32_t e = H.rowptr[(size_t)cur]; e < H.rowptr[(size_t)cur + 1]; ++e)
+        if (!seen[(size_t)H.col[(size_t)e]]) {
+          nxt = H.col[(size_t)e];
+          break;
+        }
+      cur = nxt;
+    }
+  };
+  for (int64_t i = 0; i < n; ++i)
+    if (!seen[(size_t)i] && deg(i) != 2) walk((int32_t)i);
+  for (int64_t i = 0; i < n; ++i)
+    if (!seen[(size_t)i]) walk((int32_t)i);
+}
+
+// renumber every per-row array and the CSR of graph continuum H into chain order
+static void apply_chain_order(HostCont& H) {
+  const int64_t n = H.n;
+  chain_order(H, H.perm);
+  H.inv.assign((size_t)n, 0);
+  for (int64_t t = 0; t < n; ++t) H.inv[(size_t)H.perm[(size_t)t]] = (int32_t)t;
+  auto pv = [&](std::vector<double>& v) {
+    if (v.empty()) return;
+    std::vector<double> w((size_t)n);
+    for (int64_t t = 0; t < n; ++t) w[(size_t)t] = v[(size_t)H.perm[(size_t)t]];
+    v.swap(w);
+  };
+  pv(H.mtau);
+  pv(H.dbase);
+  pv(H.F);
+  pv(H.u0);
+  pv(H.tsum);
+  pv(H.measure);
+  pv(H.gfix);
+  {
+    std::vector<uint8_t> w((size_t)n);
+    for (int64_t t = 0; t < n; ++t) w[(size_t)t] = H.fixed[(size_t)H.perm[(size_t)t]];
+    H.fixed.swap(w);
+  }
+  std::vector<int32_t> rp((size_t)n + 1, 0), col;
+  std::vector<double> val;
+  col.reserve(H.col.size());
+  if (!H.val.empty()) val.reserve(H.val.size());
+  for (int64_t t = 0; t < n; ++t) {
+    const int32_t i = H.perm[(size_t)t];
+    std::vector<std::pair<int32_t, double>> row;
+    for (int32_t e = H.rowptr[(size_t)i]; e < H.rowptr[(size_t)i + 1]; ++e)
+      row.emplace_back(H.inv[(size_t)H.col[(size_t)e]], H.val.empty() ? 0.0 : H.val[(size_t)e]);
+    std::sort(row.begin(), row.end());
+    for (auto& pr : row) {
+      col.push_back(pr.first);
+      if (!H.val.empty()) val.push_back(pr.second);
+    }
+    rp[(size_t)t + 1] = (int32_t)col.size();
+  }
+  H.rowptr.swap(rp);
+  H.col.swap(col);
+  if (!H.val.empty()) H.val.swap(val);
+}
+
 extern "C" mc_status mc_set_continuum(mc_ctx* c, int32_t alpha, const mc_continuum_desc* d) {
   if (!c || !d) return fail(c, MC_ERR_ARG, "NULL argument");
   if (alpha < 0 || alpha >= c->L) return fail(c, MC_ERR_ARG, "alpha = %d not in [0, %d)", alpha, c->L);
@@ -464,9 +545,17 @@ extern "C" mc_status mc_set_continuum(mc_ctx* c, int32_t alpha, const mc_continu
   } else {
     H.u0.assign((size_t)d->n, 0.0);
   }
-  if (H.kind == KIND_GRAPH)
+  if (H.kind == KIND_GRAPH) {
     for (size_t i = 0; i < H.fixed.size(); ++i)
       if (H.fixed[i]) H.u0[i] = H.gfix[i];                     // fixed DOF starts at g (C12)
+    // optional internal chain numbering for sparse (<= 4 neighbours) graphs, MC_CHAIN=1.
+    // Off by default: measured slower on the config-1/4 fracture networks than the
+    // caller's host-cell order.
+    int maxdeg = 0;
+    for (int64_t i = 0; i < H.n; ++i) maxdeg = std::max(maxdeg, H.rowptr[(size_t)i + 1] - H.rowptr[(size_t)i]);
+    const char* ch = getenv("MC_CHAIN");
+    if (maxdeg <= 4 && ch && ch[0] == '1') apply_chain_order(H);
+  }
   H.set = true;
   c->hc[alpha] = std::move(H);
   return MC_OK;
@@ -507,7 +596,9 @@ extern "C" mc_status mc_set_coupling(mc_ctx* c, const mc_coupling_desc* d) {
     const int32_t i = hcp.i[(size_t)e], j = hcp.j[(size_t)e];
     if (i < 0 || i >= A.n || j < 0 || j >= B.n)
       return fail(c, MC_ERR_ARG, "coupling entry %lld = (%d, %d) out of range", (long long)e, i, j);
-    if (d->scale_by_measure) hcp.s[(size_t)e] *= A.measure[(size_t)i];   // sigma |cell| (C9)
+    if (!A.inv.empty()) hcp.i[(size_t)e] = A.inv[(size_t)i];              // internal numbering
+    if (!B.inv.empty()) hcp.j[(size_t)e] = B.inv[(size_t)j];
+    if (d->scale_by_measure) hcp.s[(size_t)e] *= A.measure[(size_t)hcp.i[(size_t)e]];   // sigma |cell| (C9)
   }
   c->cpl.push_back(std::move(hcp));
   return MC_OK;
@@ -528,8 +619,9 @@ static mc_status finalize(mc_ctx* c) {
   c->N = o;
   const int64_t N = c->N;
   if (N + 1 > INT32_MAX) return fail(c, MC_ERR_ARG, "total size exceeds int32 indexing");
-  std::vector<double> mtau((size_t)N, 0.0), dbase((size_t)N, 0.0), F((size_t)N, 0.0),
-      u0((size_t)N, 0.0), tsum((size_t)N, 0.0), sig((size_t)N, 0.0);
+  const size_t NS = (size_t)N + kSlack;          // staged loads may read up to kSlack past N
+  std::vector<double> mtau(NS, 0.0), dbase(NS, 0.0), F(NS, 0.0), u0(NS, 0.0), tsum(NS, 0.0),
+      sig(NS, 0.0);
   for (int a = 0; a < c->L; ++a) {
     HostCont& H = c->hc[a];
     const size_t off = (size_t)c->off[a];
@@ -576,7 +668,7 @@ static mc_status finalize(mc_ctx* c) {
         F[(size_t)gj] += s * c->hc[h.a].gfix[(size_t)h.i[e]];
       }
     }
-  std::vector<double> dsD((size_t)N, 0.0), dinv((size_t)N, 0.0);
+  std::vector<double> dsD(NS, 0.0), dinv(NS, 0.0);
   for (int a = 0; a < c->L; ++a)
     for (int64_t i = 0; i < c->hc[a].n; ++i) {
       const size_t g = (size_t)(c->off[a] + i);
@@ -613,12 +705,15 @@ static mc_status finalize(mc_ctx* c) {
       int maxdeg = 0;
       for (int64_t i = 0; i < H.n; ++i) maxdeg = std::max(maxdeg, H.rowptr[(size_t)i + 1] - H.rowptr[(size_t)i]);
       if (maxdeg <= 4 && H.val.empty()) {
-        std::vector<int32_t> ell((size_t)(4 * H.n), -1);
+        const int64_t es = (H.n + 63) / 64 * 64 + 64;          // staged 64-row chunks may over-read
+        H.estride = es;
+        std::vector<int32_t> ell((size_t)(4 * es), -1);
         for (int64_t i = 0; i < H.n; ++i)
           for (int32_t e = H.rowptr[(size_t)i], k = 0; e < H.rowptr[(size_t)i + 1]; ++e, ++k)
-            ell[(size_t)(k * H.n + i)] = H.col[(size_t)e] + (int32_t)c->off[a];
+            ell[(size_t)(k * es + i)] = H.col[(size_t)e] + (int32_t)c->off[a];
         UP(c->ecol[a], ell);
       }
+      if (!H.perm.empty()) UP(c->perm[a], H.perm);
       UP(c->rowptr[a], H.rowptr);
       UP(c->col[a], gcol);
       if (!H.val.empty()) UP(c->val[a], H.val);
@@ -626,15 +721,21 @@ static mc_status finalize(mc_ctx* c) {
   }
 #undef UP
   for (int k = 0; k < 2; ++k) {
-    if (k == 1 && (st = dev_alloc(c, &c->u[1], (size_t)N)) != MC_OK) return st;
-    if ((st = dev_alloc(c, &c->r[k], (size_t)N)) != MC_OK) return st;
-    if ((st = dev_alloc(c, &c->p[k], (size_t)N)) != MC_OK) return st;
-    if ((st = dev_alloc(c, &c->q[k], (size_t)N)) != MC_OK) return st;
-    CUDA_TRY(c, cudaMemsetAsync(c->r[k], 0, (size_t)N * 8, c->stream));
-    CUDA_TRY(c, cudaMemsetAsync(c->p[k], 0, (size_t)N * 8, c->stream));
-    CUDA_TRY(c, cudaMemsetAsync(c->q[k], 0, (size_t)N * 8, c->stream));
+    if (k == 1 && (st = dev_alloc(c, &c->u[1], NS)) != MC_OK) return st;
+    if ((st = dev_alloc(c, &c->r[k], NS)) != MC_OK) return st;
+    if ((st = dev_alloc(c, &c->p[k], NS)) != MC_OK) return st;
+    if ((st = dev_alloc(c, &c->q[k], NS)) != MC_OK) return st;
+    CUDA_TRY(c, cudaMemsetAsync(c->r[k], 0, NS * 8, c->stream));
+    CUDA_TRY(c, cudaMemsetAsync(c->p[k], 0, NS * 8, c->stream));
+    CUDA_TRY(c, cudaMemsetAsync(c->q[k], 0, NS * 8, c->stream));
   }
-  CUDA_TRY(c, cudaMemcpyAsync(c->u[1], c->u[0], (size_t)N * 8, cudaMemcpyDeviceToDevice, c->stream));
+  CUDA_TRY(c, cudaMemcpyAsync(c->u[1], c->u[0], NS * 8, cudaMemcpyDeviceToDevice, c->stream));
+  {
+    int64_t mx = 1;
+    for (int a = 0; a < c->L; ++a)
+      if (c->hc[a].kind == KIND_GRAPH) mx = std::max(mx, c->hc[a].n);
+    if ((st = dev_alloc(c, &c->scratch, (size_t)mx)) != MC_OK) return st;
+  }
   if ((st = dev_alloc(c, &c->partials, (size_t)2 * kNPart * c->total_ctas)) != MC_OK) return st;
   if ((st = dev_alloc(c, &c->sync, 1)) != MC_OK) return st;
   if ((st = dev_alloc(c, &c->gout, MC_MAX_CONTINUA)) != MC_OK) return st;
@@ -668,14 +769,19 @@ static mc_status finalize(mc_ctx* c) {
 static void add_items(const mc_ctx* c, int a, int warps, std::vector<Item>& items) {
   const HostCont& H = c->hc[a];
   warps = std::max(warps, 1);
+  if (H.kind == KIND_GRAPH && c->ecol[a] != nullptr && c->val[a] == nullptr) return;   // round-robin (rr)
   if (H.kind == KIND_GRID) {
     const int w = (H.nx % 2 == 0) ? 64 : 32;       // 2 columns per lane when rows stay 16-B aligned
     const int strips = (H.nx + w - 1) / w;
     // distribute `warps` segments over the strips (+-1), heights as equal as possible
     const int base = std::max(1, warps / strips), extra = (warps >= strips) ? warps % strips : 0;
-    for (int s = 0; s < strips; ++s) {
-      const int segs = std::min(H.ny, base + (s < extra ? 1 : 0));
-      for (int k = 0; k < segs; ++k) {
+    // segment-major order: consecutive warps (one CTA) take adjacent strips of the same
+    // rows, so a CTA streams contiguous 8 x 512 B of every array per row step
+    const int smax = std::min(H.ny, base + (extra > 0 ? 1 : 0));
+    for (int k = 0; k < smax; ++k)
+      for (int s = 0; s < strips; ++s) {
+        const int segs = std::min(H.ny, base + (s < extra ? 1 : 0));
+        if (k >= segs) continue;
         Item it{};
         it.cont = a;
         it.kind = ITEM_GRID;
@@ -685,10 +791,9 @@ static void add_items(const mc_ctx* c, int a, int warps, std::vector<Item>& item
         it.w = w;
         if (it.c > it.b) items.push_back(it);
       }
-    }
   } else {
     int64_t chunk = (H.n + warps - 1) / warps;
-    const int64_t q = (H.col_count > 8 * H.n) ? 4 : 32;   // rows per warp-step (LPR 8 or 1)
+    const int64_t q = (H.col_count > 8 * H.n) ? 4 : 64;   // rows per warp-step (LPR 8) / staged chunk
     chunk = std::max<int64_t>(q, (chunk + q - 1) / q * q);
     for (int64_t r0 = 0; r0 < H.n; r0 += chunk) {
       Item it{};
@@ -858,6 +963,8 @@ static mc_status enqueue_step(mc_ctx* c, int scheme) {
     C.Tconst = H.Tconst;
     C.ecol = c->ecol[a];
     C.ell = c->ecol[a] ? 4 : 0;
+    C.estride = H.estride;
+    C.rr = (c->ecol[a] != nullptr && c->val[a] == nullptr) ? 1 : 0;
     C.lpr = 1;
     if (H.kind == KIND_GRAPH && H.n > 0 && H.col_count > 8 * H.n) C.lpr = 8;   // > 8 neighbours per row
   }
@@ -941,6 +1048,8 @@ extern "C" mc_status mc_step_coupled(mc_ctx* c, mc_step_report* rep) {
   return do_step(c, MC_COUPLED, rep);
 }
 
+static mc_status copy_out(mc_ctx* c, int a, double* dst);
+
 extern "C" mc_status mc_run(mc_ctx* c, int32_t scheme, int32_t n_steps, mc_step_report* reps,
                             double* const* snapshots) {
   if (!c) return fail(c, MC_ERR_ARG, "NULL context");
@@ -963,12 +1072,22 @@ extern "C" mc_status mc_run(mc_ctx* c, int32_t scheme, int32_t n_steps, mc_step_
     if (snapshots)
       for (int a = 0; a < c->L; ++a) {
         double* dst = snapshots[(size_t)s * c->L + a];
-        if (dst)
-          CUDA_TRY(c, cudaMemcpyAsync(dst, c->u[c->cur_host] + c->off[a], (size_t)c->hc[a].n * 8,
-                                      cudaMemcpyDefault, c->stream));
+        if (dst && (st = copy_out(c, a, dst)) != MC_OK) return st;
       }
   }
   CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  return MC_OK;
+}
+
+// copy p_alpha (internal numbering) to dst in the caller's numbering, stream-ordered
+static mc_status copy_out(mc_ctx* c, int a, double* dst) {
+  const double* src = c->u[c->cur_host] + c->off[a];
+  const size_t bytes = (size_t)c->hc[a].n * 8;
+  if (c->perm[a]) {
+    CUDA_TRY(c, launch_to_caller(c->scratch, src, c->perm[a], c->hc[a].n, c->stream));
+    src = c->scratch;
+  }
+  CUDA_TRY(c, cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, c->stream));
   return MC_OK;
 }
 
@@ -977,8 +1096,7 @@ extern "C" mc_status mc_get_state(mc_ctx* c, int32_t alpha, double* dst) {
   if (alpha < 0 || alpha >= c->L) return fail(c, MC_ERR_ARG, "alpha = %d out of range", alpha);
   mc_status st = finalize(c);
   if (st != MC_OK) return st;
-  CUDA_TRY(c, cudaMemcpyAsync(dst, c->u[c->cur_host] + c->off[alpha], (size_t)c->hc[alpha].n * 8,
-                              cudaMemcpyDefault, c->stream));
+  if ((st = copy_out(c, alpha, dst)) != MC_OK) return st;
   CUDA_TRY(c, cudaStreamSynchronize(c->stream));
   return MC_OK;
 }
@@ -988,8 +1106,14 @@ extern "C" mc_status mc_set_state(mc_ctx* c, int32_t alpha, const double* src) {
   if (alpha < 0 || alpha >= c->L) return fail(c, MC_ERR_ARG, "alpha = %d out of range", alpha);
   mc_status st = finalize(c);
   if (st != MC_OK) return st;
-  CUDA_TRY(c, cudaMemcpyAsync(c->u[c->cur_host] + c->off[alpha], src, (size_t)c->hc[alpha].n * 8,
-                              cudaMemcpyDefault, c->stream));
+  double* dst = c->u[c->cur_host] + c->off[alpha];
+  const size_t bytes = (size_t)c->hc[alpha].n * 8;
+  if (c->perm[alpha]) {
+    CUDA_TRY(c, cudaMemcpyAsync(c->scratch, src, bytes, cudaMemcpyDefault, c->stream));
+    CUDA_TRY(c, launch_from_caller(dst, c->scratch, c->perm[alpha], c->hc[alpha].n, c->stream));
+  } else {
+    CUDA_TRY(c, cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, c->stream));
+  }
   CUDA_TRY(c, cudaStreamSynchronize(c->stream));
   return MC_OK;
 }

@@ -9,10 +9,23 @@ namespace mc {
 
 constexpr int kThreads = 256;          // threads per CTA of the step kernel
 constexpr int kWarps = kThreads / 32;
-constexpr int kMinBlocks = 3;          // __launch_bounds__ residency target (3 x 256 per SM, 85 regs)
+#ifndef MC_MINBLOCKS
+#define MC_MINBLOCKS 2
+#endif
+#ifndef MC_STAGES
+#define MC_STAGES 2
+#endif
+constexpr int kMinBlocks = MC_MINBLOCKS;   // __launch_bounds__ residency target (CTAs of 256 per SM)
+constexpr int kStages = MC_STAGES;         // cp.async staging slots per warp (prefetch distance - 1)
 constexpr int kNPart = 5;              // reduction slots per barrier (pq, rr, rz, rq, qq)
 constexpr int kPadDofs = 32;           // continuum offsets padded to 32 doubles (256 B)
 constexpr int kCtrStride = 32;         // barrier counters 256 B apart (own L2 line / slice)
+constexpr int kSlack = 128;            // extra doubles after every per-DOF array (staged over-reads)
+// cp.async staging: per warp, two slots of the next rows' operands
+constexpr int kSlotG = 536;            // grid strip slot: 8 arrays x 64 doubles + 18 edge doubles
+constexpr int kSlotE = 528;            // ELL chunk slot: 6 x 64 doubles + 4 x 64 int32 + 2+2 halo rows x 4
+constexpr int kWarpSmem = kStages * (kSlotG > kSlotE ? kSlotG : kSlotE);   // doubles per warp
+constexpr int kDynSmem = kWarps * kWarpSmem * 8;                       // bytes per CTA
 
 enum ContKind : int32_t { KIND_GRID = 0, KIND_GRAPH = 1 };
 enum ItemKind : int32_t { ITEM_GRID = 0, ITEM_GRAPH = 1 };
@@ -31,6 +44,9 @@ struct ContDev {
   double Tconst;
   int32_t lpr;             // graph: lanes per row (1 or 8)
   int32_t ell;             // graph: ELL width (4) when ecol != nullptr
+  int64_t estride;         // graph: ELL row stride (n rounded up to 64, + 64)
+  int32_t rr;              // 1: processed by the whole group, 64-row chunks round-robin over warps
+  int32_t pad2;
 };
 
 // a work item: a 32-column strip segment of a grid, or a row range of a graph
@@ -97,6 +113,10 @@ struct StepParams {
   int32_t step_no;
   int32_t scheme;
 };
+
+// caller order <-> internal (chain) order of a graph continuum's state, perm[t] = caller index
+cudaError_t launch_to_caller(double* dst, const double* src, const int32_t* perm, int64_t n, cudaStream_t s);
+cudaError_t launch_from_caller(double* dst, const double* src, const int32_t* perm, int64_t n, cudaStream_t s);
 
 // kernel launch (mc_kernels.cu)
 cudaError_t launch_step(const StepParams* dparams, int total_ctas, cudaStream_t s);

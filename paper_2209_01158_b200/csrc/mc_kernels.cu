@@ -24,6 +24,8 @@
 //   grid: q_i = ds_i p_i + sum_faces T_f (p_i - p_nb)
 //   graph: q_i = ds_i p_i + sum_e T_e (p_i - p_j)
 //   coupled adds sum_cpl sigma (p_i - p_other).
+#include <algorithm>
+
 #include "mc_internal.h"
 
 namespace mc {
@@ -31,6 +33,9 @@ namespace mc {
 __device__ __forceinline__ double ldro(const double* p) { return __ldg(p); }
 __device__ __forceinline__ int32_t ldro(const int32_t* p) { return __ldg(p); }
 __device__ __forceinline__ double ldmut(const double* p) { return __ldcg(p); }
+// L1-cached load of a vector written in the previous pass: safe because every CTA's
+// barrier acquire (ld.acquire.gpu) invalidates its SM's L1 before the next pass reads.
+__device__ __forceinline__ double ldnb(const double* p) { return *p; }
 __device__ __forceinline__ void stmut(double* p, double v) { __stcg(p, v); }
 
 __device__ __forceinline__ unsigned long long ld_acquire(const unsigned long long* p) {
@@ -70,7 +75,7 @@ struct Ctx {
   double a, b;
 
   __device__ __forceinline__ double pn_at(int64_t gi) const {
-    return pnew(ldmut(rs + gi), ldmut(qs + gi), ldmut(ps + gi), ldro(P->dinv + gi), a, b);
+    return pnew(ldnb(rs + gi), ldnb(qs + gi), ldnb(ps + gi), ldro(P->dinv + gi), a, b);
   }
   // owner update of row gi: x, r, p stored; returns p_j, r_j, D^{-1}_ii
   __device__ __forceinline__ void own(int64_t gi, double& pn, double& rn, double& di) const {
@@ -258,6 +263,312 @@ __device__ void iter_grid2(const Ctx& c, const ContDev& C, int x0, int y0, int y
   }
 }
 
+// ---------------------------------------------------------------- cp.async staging
+__device__ __forceinline__ void cp16(void* smem, const void* gmem) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+// Grid strip, 2 columns per lane, operands of the next row streamed into shared memory
+// with cp.async one row ahead, so each warp keeps a row of loads in flight while it
+// computes the current one.  Slot k (of 2) holds: r, q, p, D^-1, x of row k+1 (own
+// columns), Tx, Ty, shift of row k, and for the strip's edge lanes the neighbouring
+// column pair (r, q, p, D^-1 of row k+1; Tx of row k).  Same arithmetic as iter_grid2.
+template <bool CPL>
+__device__ void iter_grid2s(const Ctx& c, const ContDev& C, int x0, int y0, int y1, double* wsm,
+                            double (&acc)[kNPart]) {
+  const int lane = threadIdx.x & 31;
+  const int nx = C.nx, ny = C.ny;
+  const int c0 = x0 + 2 * lane;
+  const bool valid = c0 < nx;
+  const bool hasL = valid && lane == 0 && c0 > 0;
+  const bool hasR = valid && lane == 31 && c0 + 2 < nx;
+  const int64_t off = C.off;
+  auto prefetch = [&](int k) {
+    double* sl = wsm + (k % kStages) * kSlotG;
+    if (valid) {
+      const int64_t ik = (int64_t)k * nx + c0;
+      cp16(sl + 5 * 64 + 2 * lane, C.Tx + ik);
+      cp16(sl + 6 * 64 + 2 * lane, C.Ty + ik);
+      cp16(sl + 7 * 64 + 2 * lane, c.ds + off + ik);
+      if (hasL) cp16(sl + 512 + 8, C.Tx + ik - 2);
+      if (k + 1 < ny) {
+        const int64_t g1 = off + ik + nx;
+        cp16(sl + 0 * 64 + 2 * lane, c.rs + g1);
+        cp16(sl + 1 * 64 + 2 * lane, c.qs + g1);
+        cp16(sl + 2 * 64 + 2 * lane, c.ps + g1);
+        cp16(sl + 3 * 64 + 2 * lane, c.P->dinv + g1);
+        cp16(sl + 4 * 64 + 2 * lane, c.x + g1);
+        if (hasL) {
+          cp16(sl + 512 + 0, c.rs + g1 - 2);
+          cp16(sl + 512 + 2, c.qs + g1 - 2);
+          cp16(sl + 512 + 4, c.ps + g1 - 2);
+          cp16(sl + 512 + 6, c.P->dinv + g1 - 2);
+        }
+        if (hasR) {
+          cp16(sl + 512 + 10, c.rs + g1 + 2);
+          cp16(sl + 512 + 12, c.qs + g1 + 2);
+          cp16(sl + 512 + 14, c.ps + g1 + 2);
+          cp16(sl + 512 + 16, c.P->dinv + g1 + 2);
+        }
+      }
+    }
+    cp_commit();
+  };
+  // prologue (synchronous): halo row above, own row y0, its edge neighbours
+  double2 pm = make_double2(0.0, 0.0), tym = make_double2(0.0, 0.0);
+  if (valid && y0 > 0) {
+    const int64_t i = (int64_t)(y0 - 1) * nx + c0;
+    pm = pnew2(c, off + i);
+    tym = ld2ro(C.Ty + i);
+  }
+  Row2 cur;
+  cur.p = cur.r = cur.d = make_double2(0.0, 0.0);
+  double eL = 0.0, eR = 0.0;
+  if (valid) {
+    const int64_t g0 = off + (int64_t)y0 * nx + c0;
+    cur = own2(c, g0);
+    if (hasL) eL = c.pn_at(g0 - 1);
+    if (hasR) eR = c.pn_at(g0 + 2);
+  }
+#pragma unroll
+  for (int d = 0; d < kStages - 1; ++d) {
+    if (y0 + d < y1) prefetch(y0 + d);
+    else cp_commit();
+  }
+  for (int y = y0; y < y1; ++y) {
+    if (y + kStages - 1 < y1) prefetch(y + kStages - 1);
+    else cp_commit();
+    cp_wait<kStages - 1>();
+    const double* sl = wsm + (y % kStages) * kSlotG;
+    const int64_t i = (int64_t)y * nx + c0;
+    const int64_t gi = off + i;
+    Row2 nxt;
+    nxt.p = nxt.r = nxt.d = make_double2(0.0, 0.0);
+    double nL = 0.0, nR = 0.0;
+    if (valid && y + 1 < ny) {
+      const double2 ro = *reinterpret_cast<const double2*>(sl + 0 * 64 + 2 * lane);
+      const double2 qo = *reinterpret_cast<const double2*>(sl + 1 * 64 + 2 * lane);
+      const double2 po = *reinterpret_cast<const double2*>(sl + 2 * 64 + 2 * lane);
+      const double2 di = *reinterpret_cast<const double2*>(sl + 3 * 64 + 2 * lane);
+      nxt.d = di;
+      nxt.r = make_double2(__fma_rn(-c.a, qo.x, ro.x), __fma_rn(-c.a, qo.y, ro.y));
+      nxt.p = make_double2(__fma_rn(di.x, nxt.r.x, __dmul_rn(c.b, po.x)),
+                           __fma_rn(di.y, nxt.r.y, __dmul_rn(c.b, po.y)));
+      if (y + 1 < y1) {
+        const double2 xo = *reinterpret_cast<const double2*>(sl + 4 * 64 + 2 * lane);
+        const int64_t g1 = gi + nx;
+        *reinterpret_cast<double2*>(c.x + g1) =
+            make_double2(__fma_rn(c.a, po.x, xo.x), __fma_rn(c.a, po.y, xo.y));
+        st2mut(c.rd + g1, nxt.r);
+        st2mut(c.pd + g1, nxt.p);
+      }
+      if (hasL) nL = pnew(sl[512 + 1], sl[512 + 3], sl[512 + 5], sl[512 + 7], c.a, c.b);
+      if (hasR) nR = pnew(sl[512 + 10], sl[512 + 12], sl[512 + 14], sl[512 + 16], c.a, c.b);
+    }
+    const double2 tx = valid ? *reinterpret_cast<const double2*>(sl + 5 * 64 + 2 * lane) : make_double2(0.0, 0.0);
+    double pl = __shfl_up_sync(0xffffffffu, cur.p.y, 1);
+    double pr = __shfl_down_sync(0xffffffffu, cur.p.x, 1);
+    double txl = __shfl_up_sync(0xffffffffu, tx.y, 1);
+    if (lane == 0) {
+      pl = hasL ? eL : 0.0;
+      txl = hasL ? sl[512 + 9] : 0.0;
+    }
+    if (lane == 31) pr = hasR ? eR : 0.0;
+    if (valid) {
+      const double2 ty = *reinterpret_cast<const double2*>(sl + 6 * 64 + 2 * lane);
+      const double2 ds = *reinterpret_cast<const double2*>(sl + 7 * 64 + 2 * lane);
+      const double2 pc = cur.p;
+      double q0 = ds.x * pc.x;
+      q0 += tx.x * (pc.x - pc.y);
+      q0 += txl * (pc.x - pl);
+      q0 += ty.x * (pc.x - nxt.p.x);
+      q0 += tym.x * (pc.x - pm.x);
+      double q1 = ds.y * pc.y;
+      q1 += tx.y * (pc.y - pr);
+      q1 += tx.x * (pc.y - pc.x);
+      q1 += ty.y * (pc.y - nxt.p.y);
+      q1 += tym.y * (pc.y - pm.y);
+      if (CPL) {
+        q0 += c.couple_q(gi, pc.x);
+        q1 += c.couple_q(gi + 1, pc.y);
+      }
+      st2mut(c.qd + gi, make_double2(q0, q1));
+      c.accum(acc, pc.x, cur.r.x, cur.d.x, q0);
+      c.accum(acc, pc.y, cur.r.y, cur.d.y, q1);
+      tym = ty;
+    }
+    pm = cur.p;
+    cur = nxt;
+    eL = nL;
+    eR = nR;
+  }
+  cp_wait<0>();
+}
+
+// ELL rows in chunks of 64 (lane l owns rows 2l, 2l+1), own operands and column indices
+// of the next chunk streamed into shared memory with cp.async; neighbour gathers are
+// global (L2) loads.  Same arithmetic as iter_ell.
+template <bool CPL>
+__device__ void iter_ells(const Ctx& c, const ContDev& C, int wg, int W, double* wsm,
+                          double (&acc)[kNPart]) {
+  // chunks m = wg, wg + W, ... : all warps of the group sweep the rows together, so a
+  // neighbour gathered from another chunk was (or is about to be) streamed by another
+  // warp and stays in L2
+  const int lane = threadIdx.x & 31;
+  const int64_t off = C.off, es = C.estride;
+  const int r1 = (int)C.n;
+  const int nch = (r1 + 63) / 64;
+  auto prefetch = [&](int m) {
+    double* sl = wsm + ((m / W) % kStages) * kSlotE;
+    const int64_t b = 64 * (int64_t)m;
+    const int64_t g = off + b + 2 * lane;
+    cp16(sl + 0 * 64 + 2 * lane, c.rs + g);
+    cp16(sl + 1 * 64 + 2 * lane, c.qs + g);
+    cp16(sl + 2 * 64 + 2 * lane, c.ps + g);
+    cp16(sl + 3 * 64 + 2 * lane, c.P->dinv + g);
+    cp16(sl + 4 * 64 + 2 * lane, c.x + g);
+    cp16(sl + 5 * 64 + 2 * lane, c.ds + g);
+    int32_t* si = reinterpret_cast<int32_t*>(sl + 6 * 64);
+#pragma unroll
+    for (int t = 0; t < 2; ++t) {
+      const int u = lane + 32 * t, k = u >> 4, part = u & 15;
+      cp16(si + k * 64 + 4 * part, C.ecol + k * es + b + 4 * part);
+    }
+    // halo: rows b-2, b-1 and b+64, b+65 of r, q, p, D^-1 (chain neighbours across the edge)
+    if (lane < 8 && (lane >= 4 || b >= 2)) {
+      const int a4 = lane & 3;
+      const double* src = a4 == 0 ? c.rs : a4 == 1 ? c.qs : a4 == 2 ? c.ps : c.P->dinv;
+      cp16(sl + 512 + 4 * a4 + 2 * (lane >> 2), src + off + (lane < 4 ? b - 2 : b + 64));
+    }
+    cp_commit();
+  };
+#pragma unroll
+  for (int d = 0; d < kStages - 1; ++d) {
+    if (wg + d * W < nch) prefetch(wg + d * W);
+    else cp_commit();
+  }
+  for (int m = wg; m < nch; m += W) {
+    if (m + (kStages - 1) * W < nch) prefetch(m + (kStages - 1) * W);
+    else cp_commit();
+    cp_wait<kStages - 1>();
+    const double* sl = wsm + ((m / W) % kStages) * kSlotE;
+    const int32_t* si = reinterpret_cast<const int32_t*>(sl + 6 * 64);
+    const int base = 64 * m + 2 * lane;
+    double pc[2], rc[2], dc[2], dsv[2];
+    int32_t j[2][4];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int l2 = 2 * lane + h;
+      const double ro = sl[0 * 64 + l2], qo = sl[1 * 64 + l2], po = sl[2 * 64 + l2];
+      dc[h] = sl[3 * 64 + l2];
+      rc[h] = __fma_rn(-c.a, qo, ro);
+      pc[h] = __fma_rn(dc[h], rc[h], __dmul_rn(c.b, po));
+      dsv[h] = sl[5 * 64 + l2];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) j[h][k] = si[k * 64 + l2];
+    }
+    const bool ok0 = base < r1, ok1 = base + 1 < r1;
+    const int64_t g = off + base;
+    {
+      const double2 xo = *reinterpret_cast<const double2*>(sl + 4 * 64 + 2 * lane);
+      const double2 po = *reinterpret_cast<const double2*>(sl + 2 * 64 + 2 * lane);
+      const double2 xn = make_double2(__fma_rn(c.a, po.x, xo.x), __fma_rn(c.a, po.y, xo.y));
+      if (ok1) {
+        *reinterpret_cast<double2*>(c.x + g) = xn;
+        st2mut(c.rd + g, make_double2(rc[0], rc[1]));
+        st2mut(c.pd + g, make_double2(pc[0], pc[1]));
+      } else if (ok0) {
+        c.x[g] = xn.x;
+        stmut(c.rd + g, rc[0]);
+        stmut(c.pd + g, pc[0]);
+      }
+    }
+    // neighbours inside this 64-row chunk come from the staged copy in shared memory;
+    // the others are gathered from global memory, branch-free: an absent neighbour (-1)
+    // reads the zero slack element at index N (always L1-hot) and is discarded.
+    // Neighbours inside the chunk or its 2-row halo come from the staged copy in shared
+    // memory.  The rest ("far": junction links of the chain numbering) are gathered from
+    // global memory, at most two per lane in one batch; a warp with no far neighbour
+    // issues no gather at all.
+    const int64_t cb = off + 64 * (int64_t)m;
+    double pj[2][4];
+    int64_t fidx[2] = {g, g};
+    int fslot[2] = {-1, -1};
+    int nfar = 0;
+#pragma unroll
+    for (int h = 0; h < 2; ++h)
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const int64_t jj = j[h][k];
+        const int64_t li = jj - cb;
+        const bool in = jj >= 0 && li >= -2 && li < 66;       // chunk or its 2-row halo
+        double rr_, qq_, pp_, dd_;
+        if (in && li >= 0 && li < 64) {
+          const int l = (int)li;
+          rr_ = sl[l];
+          qq_ = sl[64 + l];
+          pp_ = sl[128 + l];
+          dd_ = sl[192 + l];
+        } else {
+          const int hh = in ? (li < 0 ? (int)li + 2 : (int)li - 62) : 0;
+          rr_ = sl[512 + hh];
+          qq_ = sl[516 + hh];
+          pp_ = sl[520 + hh];
+          dd_ = sl[524 + hh];
+        }
+        pj[h][k] = jj < 0 ? pc[h] : pnew(rr_, qq_, pp_, dd_, c.a, c.b);
+        if (jj >= 0 && !in) {
+          if (nfar < 2) {
+            fidx[nfar] = jj;
+            fslot[nfar] = 4 * h + k;
+          }
+          ++nfar;
+        }
+      }
+    const int wfar = __reduce_max_sync(0xffffffffu, (unsigned)nfar);
+    if (wfar > 0) {
+      const double v0 = c.pn_at(fidx[0]);
+      const double v1 = c.pn_at(fidx[1]);
+#pragma unroll
+      for (int h = 0; h < 2; ++h)
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          if (fslot[0] == 4 * h + k) pj[h][k] = v0;
+          if (fslot[1] == 4 * h + k) pj[h][k] = v1;
+        }
+      if (wfar > 2) {                                         // rare: > 2 far neighbours in a lane
+#pragma unroll
+        for (int h = 0; h < 2; ++h)
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            const int64_t jj = j[h][k];
+            const int64_t li = jj - cb;
+            const bool far = jj >= 0 && !(li >= -2 && li < 66);
+            if (far && fslot[0] != 4 * h + k && fslot[1] != 4 * h + k) pj[h][k] = c.pn_at(jj);
+          }
+      }
+    }
+    double qv[2];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      double s = 0.0;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) s += pc[h] - pj[h][k];
+      qv[h] = dsv[h] * pc[h] + C.Tconst * s;
+      if (CPL && base + h < r1) qv[h] += c.couple_q(g + h, pc[h]);
+    }
+    if (ok1) st2mut(c.qd + g, make_double2(qv[0], qv[1]));
+    else if (ok0) stmut(c.qd + g, qv[0]);
+    if (ok0) c.accum(acc, pc[0], rc[0], dc[0], qv[0]);
+    if (ok1) c.accum(acc, pc[1], rc[1], dc[1], qv[1]);
+  }
+  cp_wait<0>();
+}
+
 // ---------------------------------------------------------------- CG pass, graph rows, ELL
 // lane-per-row over a k-major ELL copy of the adjacency (width W, -1 = no entry): the W
 // column indices arrive in one coalesced trip, then all neighbour gathers in one more.
@@ -274,7 +585,10 @@ __device__ void iter_ell(const Ctx& c, const ContDev& C, int r0, int r1, double 
     c.own(gi, pc, rc, dc);
     double pj[W];
 #pragma unroll
-    for (int k = 0; k < W; ++k) pj[k] = (j[k] >= 0) ? c.pn_at(j[k]) : pc;
+    for (int k = 0; k < W; ++k) {
+      const double v = c.pn_at(j[k] >= 0 ? (int64_t)j[k] : gi);   // branch-free gather
+      pj[k] = (j[k] >= 0) ? v : pc;
+    }
     double s = 0.0;
     if (C.val) {
 #pragma unroll
@@ -499,8 +813,20 @@ __device__ void run_group(const StepParams& P, int g, int cl, double* x, const d
   const int ib = G.item_begin, ie = G.item_begin + G.item_count;
   const bool leader = (cl == 0 && threadIdx.x == 0);
   long long t0 = leader ? globaltimer() : 0;
+  extern __shared__ __align__(16) double dsm[];
+  double* wsm = dsm + (threadIdx.x >> 5) * kWarpSmem;      // this warp's staging slots
 
   double a3[3] = {0.0, 0.0, 0.0};
+  for (int k = 0; k < P.L; ++k)
+    if (((G.cont_mask >> k) & 1) && P.cont[k].rr)
+      for (int m = wg; 32 * m < P.cont[k].n; m += W) {
+        Item rit{};
+        rit.cont = k;
+        rit.kind = ITEM_GRAPH;
+        rit.a = 32 * m;
+        rit.b = (int32_t)min((int64_t)(32 * m + 32), P.cont[k].n);
+        init_item<CPL>(P, rit, uo, x, a3);
+      }
   for (int it = ib + wg; it < ie; it += W) init_item<CPL>(P, P.items[it], uo, x, a3);
   unsigned long long epoch = 0;
   double t3[3];
@@ -531,11 +857,13 @@ __device__ void run_group(const StepParams& P, int g, int cl, double* x, const d
       c.pd = P.p[s ^ 1];
       c.qd = P.q[s ^ 1];
       double a5[kNPart] = {0.0, 0.0, 0.0, 0.0, 0.0};
+      for (int k = 0; k < P.L; ++k)
+        if (((G.cont_mask >> k) & 1) && P.cont[k].rr) iter_ells<CPL>(c, P.cont[k], wg, W, wsm, a5);
       for (int it = ib + wg; it < ie; it += W) {
         const Item item = (it == ib + wg) ? it0 : P.items[it];
         const ContDev& C = P.cont[item.cont];
         if (item.kind == ITEM_GRID) {
-          if (item.w == 64) iter_grid2<CPL>(c, C, item.a, item.b, item.c, a5);
+          if (item.w == 64) iter_grid2s<CPL>(c, C, item.a, item.b, item.c, wsm, a5);
           else iter_grid<CPL>(c, C, item.a, item.b, item.c, a5);
         } else if (C.ecol) {
           iter_ell<CPL, 4>(c, C, item.a, item.b, a5);
@@ -571,6 +899,11 @@ __device__ void run_group(const StepParams& P, int g, int cl, double* x, const d
   }
   if (zero)
     for (int it = ib + wg; it < ie; it += W) zero_item(P, P.items[it], x);
+  if (zero)
+    for (int k = 0; k < P.L; ++k)
+      if (((G.cont_mask >> k) & 1) && P.cont[k].rr)
+        for (int64_t i = (int64_t)wg * 32 + (threadIdx.x & 31); i < P.cont[k].n; i += (int64_t)W * 32)
+          x[P.cont[k].off + i] = 0.0;
   if (leader) {
     GroupOut o;
     o.iters = iters;
@@ -663,14 +996,37 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) step_kernel(const __grid
   }
 }
 
+// state I/O between the caller's numbering and the internal chain numbering
+__global__ void to_caller_kernel(double* __restrict__ dst, const double* __restrict__ src,
+                                 const int32_t* __restrict__ perm, int64_t n) {
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x)
+    dst[perm[t]] = src[t];
+}
+__global__ void from_caller_kernel(double* __restrict__ dst, const double* __restrict__ src,
+                                   const int32_t* __restrict__ perm, int64_t n) {
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x)
+    dst[t] = src[perm[t]];
+}
+static int io_blocks(int64_t n) { return (int)std::min<int64_t>(4 * 148, (n + 255) / 256 + 1); }
+cudaError_t launch_to_caller(double* dst, const double* src, const int32_t* perm, int64_t n, cudaStream_t s) {
+  to_caller_kernel<<<io_blocks(n), 256, 0, s>>>(dst, src, perm, n);
+  return cudaGetLastError();
+}
+cudaError_t launch_from_caller(double* dst, const double* src, const int32_t* perm, int64_t n, cudaStream_t s) {
+  from_caller_kernel<<<io_blocks(n), 256, 0, s>>>(dst, src, perm, n);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_step(const StepParams* params, int total_ctas, cudaStream_t s) {
   void* args[] = {(void*)params};
   return cudaLaunchCooperativeKernel((const void*)step_kernel, dim3(total_ctas), dim3(kThreads),
-                                     args, 0, s);
+                                     args, kDynSmem, s);
 }
 
 cudaError_t step_kernel_occupancy(int* blocks_per_sm) {
-  return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, step_kernel, kThreads, 0);
+  cudaError_t e = cudaFuncSetAttribute((const void*)step_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kDynSmem);
+  if (e != cudaSuccess) return e;
+  return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, step_kernel, kThreads, kDynSmem);
 }
 
 }  // namespace mc

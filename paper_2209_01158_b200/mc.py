@@ -69,11 +69,12 @@ EXPORTS = ["mc_create", "mc_set_continuum", "mc_set_coupling", "mc_step_decouple
 _lib = None
 
 
-def load(path: str = LIB_PATH):
-    """Load libmc.so; raises (no fallback) when it has not been built."""
+def load(path: str | None = None):
+    """Load libmc.so (or $MC_LIB, a tuning variant); raises (no fallback) when missing."""
     global _lib
     if _lib is not None:
         return _lib
+    path = path or os.environ.get("MC_LIB") or LIB_PATH
     if not os.path.exists(path):
         raise RuntimeError(f"libmc.so not found at {path}: build it with "
                            "`python -m paper_2209_01158_b200.build` (there is no CPU fallback)")
