@@ -32,6 +32,10 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 FALLBACK_HBM_GBS = 6650.0
+# CG tolerance per config and continuum (C13, C25): 1e-12 as BASELINE.json
+# states; config 4's matrix continuum tightened to 1e-13 because at 1e-12 it misses the
+# 1e-9 parity bar (k = exp(2Z)); its fracture solve keeps 1e-12.
+CONFIG_RTOL = {0: None, 1: None, 2: None, 3: None, 4: [1e-13, 1e-12]}
 
 
 def parse():
@@ -230,7 +234,7 @@ def main():
     scn = make(args.config)
     stream = torch.cuda.Stream()
     torch.cuda.set_stream(stream)
-    pb = Problem(scn, device=local, stream=stream)
+    pb = Problem(scn, device=local, stream=stream, rtols=CONFIG_RTOL[args.config])
     pb.byte_model = model_for(scn)
     dof = sum(pb.sizes)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
@@ -294,7 +298,7 @@ def main():
             "ms_per_step": total_ms / args.steps, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": workload_name(args.config, args.scheme), "dof": dof,
-                       "sizes": pb.sizes, "scheme": args.scheme, "rtol": 1e-12,
+                       "sizes": pb.sizes, "scheme": args.scheme, "rtol": CONFIG_RTOL[args.config] or 1e-12,
                        "cg_iters_per_step": mean_its,
                        "ms_per_solve": [sum(r["ms_solve"][a] for r in reps) / len(reps) for a in range(len(reps[0]["ms_solve"]))],
                        "l2": "flushed between timed steps (256 MiB memset)",

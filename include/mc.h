@@ -116,6 +116,9 @@ typedef struct {
   const double* edge_t;                          /* explicit T_e >= 0, or NULL            */
   double edge_geom;                              /* |E|/d when edge_t == NULL             */
   const double* dirichlet;                       /* NULL, or per cell NaN / fixed value   */
+  double rtol;                                   /* this continuum's D-scheme CG tolerance;
+                                                    <= 0: mc_options.rtol.  The coupled solve
+                                                    uses the smallest over all continua.    */
 } mc_continuum_desc;
 
 /*

@@ -14,6 +14,7 @@ from .generator import (  # noqa: F401
     CONFIGS,
     make,
     make_fine,
+    crop_fine,
     make_nlmc,
     fracture_network,
 )

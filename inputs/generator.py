@@ -212,6 +212,39 @@ def make_nlmc(nc: int = 256, *, seed: int = 3, T: float = 1.0, NT: int = 100, c=
                 between=between, dirichlet=dirichlet)
 
 
+def crop_fine(scn: dict, m: int) -> dict:
+    """The sub-square [0, m)^2 of a fine scenario: same cells (h unchanged), the k field,
+    fracture cells hosted inside, fracture edges with both ends inside, their transfer
+    coefficients; Dirichlet data on the crop's own left/right edges.  Used as a
+    full-parity stand-in for config 4 ('parity unpinned' item (i))."""
+    n = scn["n"]
+    cells = scn["fracture"]["cells"]
+    cy, cx = np.divmod(cells, n)
+    keep = (cy < m) & (cx < m)
+    new_id = np.full(len(cells), -1, dtype=np.int64)
+    new_id[keep] = np.arange(int(keep.sum()))
+    e = scn["fracture"]["edges"]
+    ek = keep[e[:, 0]] & keep[e[:, 1]]
+    edges = np.stack([new_id[e[ek, 0]], new_id[e[ek, 1]]], axis=1)
+    continua = []
+    for c in scn["continua"]:
+        c = dict(c)
+        if c["kind"] == "grid" and np.ndim(c["k"]) > 0:
+            c["k"] = np.asarray(c["k"]).reshape(n, n)[:m, :m].ravel().copy()
+        continua.append(c)
+    couplings = []
+    for cp in scn["couplings"]:
+        cp = dict(cp)
+        if cp["type"] == "embedded":
+            cp["sigma"] = np.asarray(cp["sigma"])[keep].copy()
+        couplings.append(cp)
+    if not keep.any():
+        continua = [c for c in continua if c["kind"] != "fracture"]
+        couplings = [cp for cp in couplings if cp["type"] != "embedded"]
+    return dict(scn, n=int(m), continua=continua, couplings=couplings, config_id=None,
+                fracture=dict(cells=(cy[keep] * m + cx[keep]).astype(np.int64), edges=edges))
+
+
 def make(config_id: int) -> dict:
     """The physical inputs of BASELINE.json configs[config_id]."""
     p = dict(CONFIGS[config_id])

@@ -33,6 +33,7 @@ struct HostCont {
   std::vector<int32_t> rowptr, col;            // graph, local columns
   std::vector<double> val;                     // graph per-entry T (empty -> uniform)
   double Tconst = 0.0;
+  double rtol = 0.0;                           // per-continuum CG tolerance (D-scheme)
   int64_t col_count = 0;                       // graph: stored off-diagonal entries
   int64_t estride = 0;                         // graph: ELL stride
   std::vector<int32_t> perm, inv;              // graph: internal position -> caller index, inverse
@@ -545,6 +546,9 @@ extern "C" mc_status mc_set_continuum(mc_ctx* c, int32_t alpha, const mc_continu
   } else {
     H.u0.assign((size_t)d->n, 0.0);
   }
+  if (!std::isfinite(d->rtol) || d->rtol >= 1.0)
+    return fail(c, MC_ERR_ARG, "continuum %d: rtol = %g must be < 1", alpha, d->rtol);
+  H.rtol = d->rtol > 0.0 ? d->rtol : c->opt.rtol;
   if (H.kind == KIND_GRAPH) {
     for (size_t i = 0; i < H.fixed.size(); ++i)
       if (H.fixed[i]) H.u0[i] = H.gfix[i];                     // fixed DOF starts at g (C12)
@@ -820,7 +824,9 @@ static int useful_ctas(const HostCont& H) {
 static Plan make_plan(const mc_ctx* c, int scheme) {
   Plan P;
   const int T = c->total_ctas;
-  const double tol2 = c->opt.rtol * c->opt.rtol;
+  double rmin = c->opt.rtol;
+  for (int a = 0; a < c->L; ++a) rmin = std::min(rmin, c->hc[a].rtol > 0.0 ? c->hc[a].rtol : c->opt.rtol);
+  const double tol2 = rmin * rmin;                 // coupled: the tightest tolerance
   if (scheme == MC_COUPLED) {
     P.ngroups = 1;
     P.nphases = 1;
@@ -905,7 +911,7 @@ static Plan make_plan(const mc_ctx* c, int scheme) {
   for (int a = 0; a < L; ++a) {
     Group& g = P.grp[a];
     g.cta_count = ctas[a];
-    g.tol2 = tol2;
+    g.tol2 = c->hc[a].rtol * c->hc[a].rtol;
     g.maxit = default_maxit(c, c->hc[a].n);
     g.cont_mask = 1 << a;
     g.item_begin = (int32_t)P.items.size();
@@ -969,6 +975,17 @@ static mc_status enqueue_step(mc_ctx* c, int scheme) {
     if (H.kind == KIND_GRAPH && H.n > 0 && H.col_count > 8 * H.n) C.lpr = 8;   // > 8 neighbours per row
   }
   for (int g = 0; g < cp.ngroups; ++g) P.grp[g] = cp.grp[g];
+  // resident fracture solves: alone in their group, every warp owns <= kStages chunks
+  for (int g = 0; g < cp.ngroups; ++g) {
+    const Group& G = cp.grp[g];
+    int nconts = 0;
+    for (int a = 0; a < c->L; ++a) nconts += (G.cont_mask >> a) & 1;
+    for (int a = 0; a < c->L; ++a)
+      if (((G.cont_mask >> a) & 1) && P.cont[a].rr) {
+        const int64_t nch = (c->hc[a].n + 63) / 64;
+        P.cont[a].resident = (nconts == 1 && nch <= (int64_t)kStages * G.cta_count * kWarps) ? 1 : 0;
+      }
+  }
   P.L = c->L;
   P.ngroups = cp.ngroups;
   P.nphases = cp.nphases;

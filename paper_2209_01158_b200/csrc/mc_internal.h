@@ -46,7 +46,7 @@ struct ContDev {
   int32_t ell;             // graph: ELL width (4) when ecol != nullptr
   int64_t estride;         // graph: ELL row stride (n rounded up to 64, + 64)
   int32_t rr;              // 1: processed by the whole group, 64-row chunks round-robin over warps
-  int32_t pad2;
+  int32_t resident;        // rr + every warp owns <= kStages chunks: state stays in shared memory
 };
 
 // a work item: a 32-column strip segment of a grid, or a row range of a graph

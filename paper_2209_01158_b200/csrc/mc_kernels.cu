@@ -569,6 +569,155 @@ __device__ void iter_ells(const Ctx& c, const ContDev& C, int wg, int W, double*
   cp_wait<0>();
 }
 
+// Resident variant of iter_ells for latency-bound graphs (every warp owns <= kStages
+// chunks): the chunks' r, q, p, x, D^-1, shift and ELL columns live in
+// this warp's shared-memory slots for the whole solve, so an iteration reads no
+// streamed operand from memory; in-chunk neighbours read the new p_j straight from
+// shared memory; only neighbours owned by other warps are gathered (from the previous
+// iteration's r, q, p in global memory, recomputed with pnew as everywhere else).
+// r, p, q are still stored to global every iteration for those gathers; x is flushed
+// at the end of the solve (flush_ells_res).
+template <bool CPL>
+__device__ void iter_ells_res(const Ctx& c, const ContDev& C, int wg, int W, double* wsm, bool first,
+                              double (&acc)[kNPart]) {
+  const int lane = threadIdx.x & 31;
+  const int64_t off = C.off, es = C.estride;
+  const int r1 = (int)C.n;
+  const int nch = (r1 + 63) / 64;
+  if (first) {
+    for (int m = wg, t = 0; m < nch; m += W, ++t) {
+      double* sl = wsm + t * kSlotE;
+      const int64_t b = 64 * (int64_t)m, g = off + b + 2 * lane;
+      cp16(sl + 0 * 64 + 2 * lane, c.rs + g);
+      cp16(sl + 1 * 64 + 2 * lane, c.qs + g);
+      cp16(sl + 2 * 64 + 2 * lane, c.ps + g);
+      cp16(sl + 3 * 64 + 2 * lane, c.P->dinv + g);
+      cp16(sl + 4 * 64 + 2 * lane, c.x + g);
+      cp16(sl + 5 * 64 + 2 * lane, c.ds + g);
+      int32_t* si = reinterpret_cast<int32_t*>(sl + 6 * 64);
+#pragma unroll
+      for (int u2 = 0; u2 < 2; ++u2) {
+        const int u = lane + 32 * u2, k = u >> 4, part = u & 15;
+        cp16(si + k * 64 + 4 * part, C.ecol + k * es + b + 4 * part);
+      }
+    }
+    cp_commit();
+    cp_wait<0>();
+    __syncwarp();
+  }
+  for (int m = wg, t = 0; m < nch; m += W, ++t) {
+    double* sl = wsm + t * kSlotE;
+    const int32_t* si = reinterpret_cast<const int32_t*>(sl + 6 * 64);
+    const int base = 64 * m + 2 * lane;
+    const int64_t g = off + base;
+    const int64_t cb = off + 64 * (int64_t)m;
+    const bool ok0 = base < r1, ok1 = base + 1 < r1;
+    double pc[2], rc[2], dc[2], dsv[2];
+    int32_t j[2][4];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int l2 = 2 * lane + h;
+      const double ro = sl[l2], qo = sl[64 + l2], po = sl[128 + l2];
+      dc[h] = sl[192 + l2];
+      rc[h] = __fma_rn(-c.a, qo, ro);
+      pc[h] = __fma_rn(dc[h], rc[h], __dmul_rn(c.b, po));
+      dsv[h] = sl[320 + l2];
+      sl[256 + l2] = __fma_rn(c.a, po, sl[256 + l2]);           // x (flushed at the end)
+#pragma unroll
+      for (int k = 0; k < 4; ++k) j[h][k] = si[k * 64 + l2];
+    }
+    // far neighbours: issue the gathers first (previous iteration's r, q, p in global)
+    int64_t fidx[2] = {g, g};
+    int fslot[2] = {-1, -1};
+    int nfar = 0;
+#pragma unroll
+    for (int h = 0; h < 2; ++h)
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const int64_t jj = j[h][k];
+        const int64_t li = jj - cb;
+        if (jj >= 0 && !(li >= 0 && li < 64)) {
+          if (nfar < 2) {
+            fidx[nfar] = jj;
+            fslot[nfar] = 4 * h + k;
+          }
+          ++nfar;
+        }
+      }
+    const int wfar = __reduce_max_sync(0xffffffffu, (unsigned)nfar);
+    double v0 = 0.0, v1 = 0.0;
+    if (wfar > 0) {
+      v0 = c.pn_at(fidx[0]);
+      v1 = c.pn_at(fidx[1]);
+    }
+    // publish: own r_j, p_j into the slots (p_j is what in-chunk neighbours need)
+    __syncwarp();
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      sl[2 * lane + h] = rc[h];
+      sl[128 + 2 * lane + h] = pc[h];
+    }
+    if (ok1) {
+      st2mut(c.rd + g, make_double2(rc[0], rc[1]));
+      st2mut(c.pd + g, make_double2(pc[0], pc[1]));
+    } else if (ok0) {
+      stmut(c.rd + g, rc[0]);
+      stmut(c.pd + g, pc[0]);
+    }
+    __syncwarp();
+    double pj[2][4];
+#pragma unroll
+    for (int h = 0; h < 2; ++h)
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const int64_t jj = j[h][k];
+        const int64_t li = jj - cb;
+        const bool in = jj >= 0 && li >= 0 && li < 64;
+        double v = in ? sl[128 + (int)li] : pc[h];
+        if (fslot[0] == 4 * h + k) v = v0;
+        else if (fslot[1] == 4 * h + k) v = v1;
+        pj[h][k] = v;
+      }
+    if (wfar > 2) {
+#pragma unroll
+      for (int h = 0; h < 2; ++h)
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const int64_t jj = j[h][k];
+          const int64_t li = jj - cb;
+          if (jj >= 0 && !(li >= 0 && li < 64) && fslot[0] != 4 * h + k && fslot[1] != 4 * h + k)
+            pj[h][k] = c.pn_at(jj);
+        }
+    }
+    double qv[2];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      double s = 0.0;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) s += pc[h] - pj[h][k];
+      qv[h] = dsv[h] * pc[h] + C.Tconst * s;
+    }
+    sl[64 + 2 * lane] = qv[0];
+    sl[64 + 2 * lane + 1] = qv[1];
+    if (ok1) st2mut(c.qd + g, make_double2(qv[0], qv[1]));
+    else if (ok0) stmut(c.qd + g, qv[0]);
+    if (ok0) c.accum(acc, pc[0], rc[0], dc[0], qv[0]);
+    if (ok1) c.accum(acc, pc[1], rc[1], dc[1], qv[1]);
+  }
+}
+
+__device__ void flush_ells_res(const ContDev& C, int wg, int W, const double* wsm, double* x) {
+  const int lane = threadIdx.x & 31;
+  const int nch = (int)((C.n + 63) / 64);
+  for (int m = wg, t = 0; m < nch; m += W, ++t) {
+    const double* sl = wsm + t * kSlotE;
+    for (int h = 0; h < 2; ++h) {
+      const int64_t i = 64 * (int64_t)m + 2 * lane + h;
+      if (i < C.n) x[C.off + i] = sl[256 + 2 * lane + h];
+    }
+  }
+}
+
 // ---------------------------------------------------------------- CG pass, graph rows, ELL
 // lane-per-row over a k-major ELL copy of the adjacency (width W, -1 = no entry): the W
 // column indices arrive in one coalesced trip, then all neighbour gathers in one more.
@@ -834,6 +983,7 @@ __device__ void run_group(const StepParams& P, int g, int cl, double* x, const d
   const double bb = t3[0];
   double rr = t3[1];
   int64_t iters = 0;
+  int64_t passes = 0;
   int status = MC_OK;
   bool zero = false;
   if (bb == 0.0) {
@@ -858,7 +1008,10 @@ __device__ void run_group(const StepParams& P, int g, int cl, double* x, const d
       c.qd = P.q[s ^ 1];
       double a5[kNPart] = {0.0, 0.0, 0.0, 0.0, 0.0};
       for (int k = 0; k < P.L; ++k)
-        if (((G.cont_mask >> k) & 1) && P.cont[k].rr) iter_ells<CPL>(c, P.cont[k], wg, W, wsm, a5);
+        if (((G.cont_mask >> k) & 1) && P.cont[k].rr) {
+          if (P.cont[k].resident) iter_ells_res<CPL>(c, P.cont[k], wg, W, wsm, j == 0, a5);
+          else iter_ells<CPL>(c, P.cont[k], wg, W, wsm, a5);
+        }
       for (int it = ib + wg; it < ie; it += W) {
         const Item item = (it == ib + wg) ? it0 : P.items[it];
         const ContDev& C = P.cont[item.cont];
@@ -875,6 +1028,7 @@ __device__ void run_group(const StepParams& P, int g, int cl, double* x, const d
       }
       double t5[kNPart];
       group_allreduce<kNPart>(P, g, cl, epoch, a5, t5);
+      passes = j + 1;
       rr = t5[1];
       if (j > 0 && rr <= G.tol2 * bb) {
         iters = j;
@@ -897,6 +1051,9 @@ __device__ void run_group(const StepParams& P, int g, int cl, double* x, const d
       c.b = rz_next / rz;
     }
   }
+  if (passes > 0)
+    for (int k = 0; k < P.L; ++k)
+      if (((G.cont_mask >> k) & 1) && P.cont[k].rr && P.cont[k].resident) flush_ells_res(P.cont[k], wg, W, wsm, x);
   if (zero)
     for (int it = ib + wg; it < ie; it += W) zero_item(P, P.items[it], x);
   if (zero)

@@ -41,7 +41,7 @@ class mc_continuum_desc(C.Structure):
                 ("nx", _i32), ("ny", _i32), ("h", _d), ("bc_left", _i32), ("bc_right", _i32),
                 ("g_left", _d), ("g_right", _d),
                 ("measure", _pd), ("measure_const", _d), ("n_edges", _i64), ("edge_i", _pi),
-                ("edge_j", _pi), ("edge_t", _pd), ("edge_geom", _d), ("dirichlet", _pd)]
+                ("edge_j", _pi), ("edge_t", _pd), ("edge_geom", _d), ("dirichlet", _pd), ("rtol", _d)]
 
 
 class mc_coupling_desc(C.Structure):
@@ -127,7 +127,8 @@ class Problem:
     """
 
     def __init__(self, scn, tau=None, rtol=1e-12, maxit=0, ctas=0, device=0, stream=None,
-                 host_inputs=False):
+                 host_inputs=False, rtols=None):
+        """rtols: optional per-continuum CG tolerances (D-scheme), default rtol for all."""
         import torch
         self.lib = load()
         self.torch = torch
@@ -144,6 +145,9 @@ class Problem:
         self.host_inputs = host_inputs
         conts, cpls = self._descs(scn)
         self.L = len(conts)
+        if rtols is not None:
+            for d, t in zip(conts, rtols):
+                d.rtol = float(t)
         self._check(self.lib.mc_create(C.byref(self.ctx), self.L, C.byref(opt)), create=True)
         for a, d in enumerate(conts):
             self._check(self.lib.mc_set_continuum(self.ctx, a, C.byref(d)))

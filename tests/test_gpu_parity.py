@@ -10,12 +10,13 @@ import math
 import numpy as np
 import pytest
 
-from inputs import CONFIGS, make, make_fine, make_nlmc
+from inputs import CONFIGS, crop_fine, make, make_fine, make_nlmc
 from oracle import assemble as asm
 from oracle import schemes
 
 pytestmark = pytest.mark.gpu
 TOL = 1e-9
+CONFIG_RTOL = {0: None, 1: None, 2: None, 3: None, 4: [1e-13, 1e-12]}   # per continuum, C25
 
 
 @pytest.fixture(scope="module")
@@ -262,32 +263,36 @@ def test_argument_errors(torch_cuda):
 
 
 # ---------------------------------------------------------------- full sizes: properties
-def _residual_check(scn, steps, scheme="D"):
-    """The GPU iterate satisfies the ORACLE's equations: ||K_a u^{n+1} - b_a(u^n)|| / ||b_a||."""
+def _residual_check(scn, steps, scheme="D", tol=1e-6, rtols=None):
+    """At full size, where a sparse factorisation is out of reach: the GPU iterate
+    satisfies the ORACLE's equations, ||K_a u^{n+1} - b_a(u^n)|| <= tol ||b_a||, with
+    the oracle's own operator evaluated in flux form (oracle.assemble.FluxForm) and its
+    own right-hand side from the GPU's previous state.  Bound: the true residual of a CG
+    iterate floors at ~1e-8..1e-7 for the fracture systems (residual gap of fp64 CG with
+    T_f/sigma ~ 1e7, reading C13), so 1e-6 here; forward errors are pinned by the
+    full-trajectory and cropped stand-in tests."""
     from paper_2209_01158_b200 import Problem
     sys_ = asm.assemble(scn)
     tau = scn["T"] / scn["NT"]
-    ds = schemes.DScheme.__new__(schemes.DScheme)
-    ds.sys, ds.tau = sys_, tau
-    ds.A0, ds.A1 = schemes.split_D(sys_)
-    import scipy.sparse as sp
-    K0 = sp.csr_matrix(sp.diags(sys_.M / tau) + ds.A0)
-    pb = Problem(scn)
+    mt = sys_.M / tau
+    _, A1 = schemes.split_D(sys_)
+    ops = [sys_.flux.block_op(sys_.block(a), mt, "D") for a in range(sys_.L)]
+    pb = Problem(scn, rtols=rtols)
     u = sys_.u0.copy()
     worst = []
     for _ in range(steps):
         rep = pb.step(scheme)
         new = np.concatenate([t.cpu().numpy() for t in pb.state()])
-        b = ds.rhs(u)
+        b = mt * u + sys_.F - A1 @ u                  # D-scheme RHS, PAPER.md:477-486
         for a in range(sys_.L):
             s = sys_.block(a)
             nb = np.linalg.norm(b[s])
             if nb == 0:
                 assert np.array_equal(new[s], np.zeros_like(new[s]))
                 continue
-            res = np.linalg.norm(K0[s, s] @ new[s] - b[s]) / nb
+            res = np.linalg.norm(ops[a].apply(new[s]) - b[s]) / nb
             worst.append(res)
-            assert res <= 1e-6, (a, res, rep)
+            assert res <= tol, (a, res, rep)
         u = new
     pb.close()
     return worst
@@ -295,9 +300,23 @@ def _residual_check(scn, steps, scheme="D"):
 
 @pytest.mark.slow
 def test_config2_full_size_residuals(torch_cuda):
-    _residual_check(make(2), 3)
+    w = _residual_check(make(2), 3)
+    print("config2 residuals", w)
 
 
 @pytest.mark.slow
 def test_config4_full_size_residuals(torch_cuda):
-    _residual_check(make(4), 2)
+    w = _residual_check(make(4), 2, rtols=CONFIG_RTOL[4])
+    print("config4 residuals", w)
+
+
+@pytest.mark.parametrize("scheme", ["D", "coupled"])
+def test_config4_cropped_standin(torch_cuda, scheme):
+    """Config 4's own k field and fracture network on its [0,512)^2 corner (h = 1/8192
+    kept), full trajectory parity against the oracle.  rtol 1e-13: with k = exp(2Z) the
+    matrix block's forward error at rtol 1e-12 is 1.7e-9 (measured), so config 4's matrix
+    continuum runs at 1e-13 (fracture 1e-12), disclosed in DESIGN.md (C25), as in bench.py."""
+    scn = crop_fine(make(4), 512)
+    got, _ = gpu_traj(scn, scheme, 4, rtols=CONFIG_RTOL[4])
+    ref = oracle_traj(scn, scheme, 4)
+    assert_parity(got, ref)
