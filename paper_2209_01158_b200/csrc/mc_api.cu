@@ -711,10 +711,17 @@ static mc_status finalize(mc_ctx* c) {
       if (maxdeg <= 4 && H.val.empty()) {
         const int64_t es = (H.n + 63) / 64 * 64 + 64;          // staged 64-row chunks may over-read
         H.estride = es;
+        // ELL entries pre-classified against the static 64-row chunk of their row:
+        //   -1 none; -2-w: window slot w = j - chunk_start + 2 in [0, 68) (the chunk and its
+        //   2-row halo on each side, staged in shared memory); >= 0: global index (far)
         std::vector<int32_t> ell((size_t)(4 * es), -1);
-        for (int64_t i = 0; i < H.n; ++i)
-          for (int32_t e = H.rowptr[(size_t)i], k = 0; e < H.rowptr[(size_t)i + 1]; ++e, ++k)
-            ell[(size_t)(k * es + i)] = H.col[(size_t)e] + (int32_t)c->off[a];
+        for (int64_t i = 0; i < H.n; ++i) {
+          const int64_t b = i / 64 * 64;
+          for (int32_t e = H.rowptr[(size_t)i], k = 0; e < H.rowptr[(size_t)i + 1]; ++e, ++k) {
+            const int64_t j = H.col[(size_t)e], w = j - b + 2;
+            ell[(size_t)(k * es + i)] = (w >= 0 && w < 68) ? (int32_t)(-2 - w) : (int32_t)(j + c->off[a]);
+          }
+        }
         UP(c->ecol[a], ell);
       }
       if (!H.perm.empty()) UP(c->perm[a], H.perm);

@@ -15,6 +15,9 @@ constexpr int kWarps = kThreads / 32;
 #ifndef MC_STAGES
 #define MC_STAGES 2
 #endif
+#ifndef MC_TMA
+#define MC_TMA 1                           // stage with TMA bulk copies (1) or per-lane cp.async (0)
+#endif
 constexpr int kMinBlocks = MC_MINBLOCKS;   // __launch_bounds__ residency target (CTAs of 256 per SM)
 constexpr int kStages = MC_STAGES;         // cp.async staging slots per warp (prefetch distance - 1)
 constexpr int kNPart = 5;              // reduction slots per barrier (pq, rr, rz, rq, qq)
@@ -23,9 +26,13 @@ constexpr int kCtrStride = 32;         // barrier counters 256 B apart (own L2 l
 constexpr int kSlack = 128;            // extra doubles after every per-DOF array (staged over-reads)
 // cp.async staging: per warp, two slots of the next rows' operands
 constexpr int kSlotG = 536;            // grid strip slot: 8 arrays x 64 doubles + 18 edge doubles
-constexpr int kSlotE = 528;            // ELL chunk slot: 6 x 64 doubles + 4 x 64 int32 + 2+2 halo rows x 4
-constexpr int kWarpSmem = kStages * (kSlotG > kSlotE ? kSlotG : kSlotE);   // doubles per warp
-constexpr int kDynSmem = kWarps * kWarpSmem * 8;                       // bytes per CTA
+constexpr int kSlotE = 528;            // ELL chunk slot: r, q, p, D^-1 windows (68), x, shift (64), 4 x 64 int32 codes
+constexpr int kStagesE = 3;                // ELL pass: load -> gather -> compute pipeline
+constexpr int kPnBuf = 72;                 // ELL pass: new p of the chunk window (68) per warp
+constexpr int kWarpSmem = ((kStages * kSlotG > kStagesE * kSlotE) ? kStages * kSlotG : kStagesE * kSlotE) + kPnBuf;
+// bytes per CTA: staging slots, then one mbarrier per slot per warp, then a parity word per warp
+constexpr int kNBars = (kStages > kStagesE) ? kStages : kStagesE;   // mbarriers per warp
+constexpr int kDynSmem = kWarps * kWarpSmem * 8 + kWarps * kNBars * 8 + kWarps * 8;
 
 enum ContKind : int32_t { KIND_GRID = 0, KIND_GRAPH = 1 };
 enum ItemKind : int32_t { ITEM_GRID = 0, ITEM_GRAPH = 1 };
@@ -40,7 +47,7 @@ struct ContDev {
   const int32_t* rowptr;   // graph: [n+1], local
   const int32_t* col;      // graph: GLOBAL column indices
   const double* val;       // graph: per-entry T, or nullptr -> Tconst
-  const int32_t* ecol;     // graph: ELL copy of col, [ell][n] (k-major, -1 = none), or nullptr
+  const int32_t* ecol;     // graph: ELL codes [4][estride] (k-major): -1 none, -2-w window slot, >=0 global
   double Tconst;
   int32_t lpr;             // graph: lanes per row (1 or 8)
   int32_t ell;             // graph: ELL width (4) when ecol != nullptr

@@ -272,14 +272,59 @@ __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_grou
 template <int N>
 __device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
+// TMA bulk copies (cp.async.bulk, one issuing lane per warp) tracked by an mbarrier per
+// staging slot; the parity of every slot's barrier lives in a per-warp word (`ph`).
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n WAIT%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra WAIT%=;\n}" ::"r"(
+          smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
+// per-warp staging state: slots of doubles, one mbarrier per slot, slot parities
+struct Stage {
+  double* wsm;
+  uint64_t* bars;
+  unsigned* ph;
+  // lane 0 of the warp: begin filling slot t with `bytes` of bulk copies
+  __device__ __forceinline__ void begin(int t, unsigned bytes) const {
+    fence_proxy_async();
+    mbar_expect_tx(bars + t, bytes);
+  }
+  // all lanes: wait until slot t is filled, flip its parity
+  __device__ __forceinline__ void wait(int t) const {
+    const unsigned par = (*ph >> t) & 1u;
+    mbar_wait(bars + t, par);
+    __syncwarp();
+    if ((threadIdx.x & 31) == 0) *ph ^= (1u << t);
+    __syncwarp();
+  }
+};
+
 // Grid strip, 2 columns per lane, operands of the next row streamed into shared memory
 // with cp.async one row ahead, so each warp keeps a row of loads in flight while it
 // computes the current one.  Slot k (of 2) holds: r, q, p, D^-1, x of row k+1 (own
 // columns), Tx, Ty, shift of row k, and for the strip's edge lanes the neighbouring
 // column pair (r, q, p, D^-1 of row k+1; Tx of row k).  Same arithmetic as iter_grid2.
 template <bool CPL>
-__device__ void iter_grid2s(const Ctx& c, const ContDev& C, int x0, int y0, int y1, double* wsm,
+__device__ void iter_grid2s(const Ctx& c, const ContDev& C, int x0, int y0, int y1, const Stage& st,
                             double (&acc)[kNPart]) {
+  double* wsm = st.wsm;
   const int lane = threadIdx.x & 31;
   const int nx = C.nx, ny = C.ny;
   const int c0 = x0 + 2 * lane;
@@ -287,6 +332,48 @@ __device__ void iter_grid2s(const Ctx& c, const ContDev& C, int x0, int y0, int 
   const bool hasL = valid && lane == 0 && c0 > 0;
   const bool hasR = valid && lane == 31 && c0 + 2 < nx;
   const int64_t off = C.off;
+#if MC_TMA
+  const int vl = (nx - x0) / 2 < 32 ? (nx - x0) / 2 : 32;      // valid lanes of this strip
+  const unsigned rowb = 16u * (unsigned)vl;
+  const bool sL = x0 > 0, sR = x0 + 64 < nx;                    // strip has left / right neighbours
+  auto prefetch = [&](int k) {
+    const int t = k % kStages;
+    double* sl = wsm + t * kSlotG;
+    __syncwarp();
+    if (lane == 0) {
+      const int64_t ik = (int64_t)k * nx + x0;
+      const bool nxt = k + 1 < ny;
+      const unsigned bytes = 3u * rowb + (sL ? 16u : 0u) +
+                             (nxt ? 5u * rowb + (sL ? 64u : 0u) + (sR ? 64u : 0u) : 0u);
+      st.begin(t, bytes);
+      uint64_t* bar = st.bars + t;
+      bulk_g2s(sl + 5 * 64, C.Tx + ik, rowb, bar);
+      bulk_g2s(sl + 6 * 64, C.Ty + ik, rowb, bar);
+      bulk_g2s(sl + 7 * 64, c.ds + off + ik, rowb, bar);
+      if (sL) bulk_g2s(sl + 512 + 8, C.Tx + ik - 2, 16, bar);
+      if (nxt) {
+        const int64_t g1 = off + ik + nx;
+        bulk_g2s(sl + 0 * 64, c.rs + g1, rowb, bar);
+        bulk_g2s(sl + 1 * 64, c.qs + g1, rowb, bar);
+        bulk_g2s(sl + 2 * 64, c.ps + g1, rowb, bar);
+        bulk_g2s(sl + 3 * 64, c.P->dinv + g1, rowb, bar);
+        bulk_g2s(sl + 4 * 64, c.x + g1, rowb, bar);
+        if (sL) {
+          bulk_g2s(sl + 512 + 0, c.rs + g1 - 2, 16, bar);
+          bulk_g2s(sl + 512 + 2, c.qs + g1 - 2, 16, bar);
+          bulk_g2s(sl + 512 + 4, c.ps + g1 - 2, 16, bar);
+          bulk_g2s(sl + 512 + 6, c.P->dinv + g1 - 2, 16, bar);
+        }
+        if (sR) {
+          bulk_g2s(sl + 512 + 10, c.rs + g1 + 64, 16, bar);
+          bulk_g2s(sl + 512 + 12, c.qs + g1 + 64, 16, bar);
+          bulk_g2s(sl + 512 + 14, c.ps + g1 + 64, 16, bar);
+          bulk_g2s(sl + 512 + 16, c.P->dinv + g1 + 64, 16, bar);
+        }
+      }
+    }
+  };
+#else
   auto prefetch = [&](int k) {
     double* sl = wsm + (k % kStages) * kSlotG;
     if (valid) {
@@ -318,6 +405,7 @@ __device__ void iter_grid2s(const Ctx& c, const ContDev& C, int x0, int y0, int 
     }
     cp_commit();
   };
+#endif
   // prologue (synchronous): halo row above, own row y0, its edge neighbours
   double2 pm = make_double2(0.0, 0.0), tym = make_double2(0.0, 0.0);
   if (valid && y0 > 0) {
@@ -337,12 +425,18 @@ __device__ void iter_grid2s(const Ctx& c, const ContDev& C, int x0, int y0, int 
 #pragma unroll
   for (int d = 0; d < kStages - 1; ++d) {
     if (y0 + d < y1) prefetch(y0 + d);
+#if !MC_TMA
     else cp_commit();
+#endif
   }
   for (int y = y0; y < y1; ++y) {
     if (y + kStages - 1 < y1) prefetch(y + kStages - 1);
+#if MC_TMA
+    st.wait(y % kStages);
+#else
     else cp_commit();
     cp_wait<kStages - 1>();
+#endif
     const double* sl = wsm + (y % kStages) * kSlotG;
     const int64_t i = (int64_t)y * nx + c0;
     const int64_t gi = off + i;
@@ -409,74 +503,142 @@ __device__ void iter_grid2s(const Ctx& c, const ContDev& C, int x0, int y0, int 
   cp_wait<0>();
 }
 
-// ELL rows in chunks of 64 (lane l owns rows 2l, 2l+1), own operands and column indices
-// of the next chunk streamed into shared memory with cp.async; neighbour gathers are
-// global (L2) loads.  Same arithmetic as iter_ell.
+// ELL rows in 64-row chunks swept round-robin by the group's warps (lane l owns rows
+// 2l, 2l+1 of a chunk); three-stage software pipeline per warp:
+//   A  TMA bulk copies of chunk m+2W: r, q, p, D^-1 over the chunk and a 2-row halo on
+//      each side (68-row window), x, shift, and the 4 ELL codes;
+//   B  for chunk m+W (landed): gather the "far" neighbours (code >= 0: neither in the
+//      chunk nor in its halo, at most 2 per lane per batch) — their p_j recomputed from
+//      the previous iteration's r, q, p, stable for the whole pass;
+//   C  chunk m: new p of every window row into a per-warp buffer, then q from it.
+// ELL codes are pre-classified on the host against the static chunk (mc_api.cu).
+// Neighbours in another chunk were (or are about to be) streamed by another warp of
+// the sweep, so the far gathers hit L2.
+struct FarG {
+  double r0, q0, p0, d0, r1, q1, p1, d1;   // raw previous-iteration values (consumed later,
+                                           // so the gather latency overlaps other work)
+  int s0, s1;      // 4*h + k slot the value belongs to, -1 = none
+  int more;        // warp-uniform: some lane has > 2 far neighbours in this chunk
+  __device__ __forceinline__ double v0(const Ctx& c) const { return pnew(r0, q0, p0, d0, c.a, c.b); }
+  __device__ __forceinline__ double v1(const Ctx& c) const { return pnew(r1, q1, p1, d1, c.a, c.b); }
+};
+
+__device__ __forceinline__ void ell_codes(const double* sl, int lane, int32_t (&j)[2][4]) {
+  const int32_t* si = reinterpret_cast<const int32_t*>(sl + 400);
+#pragma unroll
+  for (int h = 0; h < 2; ++h)
+#pragma unroll
+    for (int k = 0; k < 4; ++k) j[h][k] = si[k * 64 + 2 * lane + h];
+}
+
+__device__ __forceinline__ FarG far_gather(const Ctx& c, const double* sl, int lane, int64_t g) {
+  int32_t j[2][4];
+  ell_codes(sl, lane, j);
+  FarG f;
+  f.s0 = f.s1 = -1;
+  int64_t i0 = g, i1 = g;
+  int nfar = 0;
+#pragma unroll
+  for (int h = 0; h < 2; ++h)
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+      if (j[h][k] >= 0) {
+        if (nfar == 0) {
+          i0 = j[h][k];
+          f.s0 = 4 * h + k;
+        } else if (nfar == 1) {
+          i1 = j[h][k];
+          f.s1 = 4 * h + k;
+        }
+        ++nfar;
+      }
+  const unsigned wfar = __reduce_max_sync(0xffffffffu, (unsigned)nfar);
+  f.more = wfar > 2;
+  if (wfar > 0) {
+    f.r0 = ldnb(c.rs + i0);
+    f.q0 = ldnb(c.qs + i0);
+    f.p0 = ldnb(c.ps + i0);
+    f.d0 = ldro(c.P->dinv + i0);
+    f.r1 = ldnb(c.rs + i1);
+    f.q1 = ldnb(c.qs + i1);
+    f.p1 = ldnb(c.ps + i1);
+    f.d1 = ldro(c.P->dinv + i1);
+  } else {
+    f.r0 = f.q0 = f.p0 = f.d0 = f.r1 = f.q1 = f.p1 = f.d1 = 0.0;
+  }
+  return f;
+}
+
 template <bool CPL>
-__device__ void iter_ells(const Ctx& c, const ContDev& C, int wg, int W, double* wsm,
+__device__ void iter_ells(const Ctx& c, const ContDev& C, int wg, int W, const Stage& st,
                           double (&acc)[kNPart]) {
-  // chunks m = wg, wg + W, ... : all warps of the group sweep the rows together, so a
-  // neighbour gathered from another chunk was (or is about to be) streamed by another
-  // warp and stays in L2
+  double* wsm = st.wsm;
+  double* pnb = wsm + kWarpSmem - kPnBuf;                      // new p of the window rows
   const int lane = threadIdx.x & 31;
   const int64_t off = C.off, es = C.estride;
   const int r1 = (int)C.n;
   const int nch = (r1 + 63) / 64;
+  auto tix = [&](int m) { return (m / W) % kStagesE; };
+  auto slot = [&](int m) { return wsm + tix(m) * kSlotE; };
   auto prefetch = [&](int m) {
-    double* sl = wsm + ((m / W) % kStages) * kSlotE;
-    const int64_t b = 64 * (int64_t)m;
-    const int64_t g = off + b + 2 * lane;
-    cp16(sl + 0 * 64 + 2 * lane, c.rs + g);
-    cp16(sl + 1 * 64 + 2 * lane, c.qs + g);
-    cp16(sl + 2 * 64 + 2 * lane, c.ps + g);
-    cp16(sl + 3 * 64 + 2 * lane, c.P->dinv + g);
-    cp16(sl + 4 * 64 + 2 * lane, c.x + g);
-    cp16(sl + 5 * 64 + 2 * lane, c.ds + g);
-    int32_t* si = reinterpret_cast<int32_t*>(sl + 6 * 64);
-#pragma unroll
-    for (int t = 0; t < 2; ++t) {
-      const int u = lane + 32 * t, k = u >> 4, part = u & 15;
-      cp16(si + k * 64 + 4 * part, C.ecol + k * es + b + 4 * part);
+    const int t = tix(m);
+    double* sl = wsm + t * kSlotE;
+    __syncwarp();
+    if (lane == 0) {
+      const int64_t b = 64 * (int64_t)m;
+      const int64_t g = off + b;
+      const bool full = g >= 2;                                 // window start in bounds
+      const unsigned wb = full ? 544u : 528u;
+      st.begin(t, 4u * wb + 2u * 512u + 4u * 256u);
+      uint64_t* bar = st.bars + t;
+      const double* src4[4] = {c.rs, c.qs, c.ps, c.P->dinv};
+      for (int a4 = 0; a4 < 4; ++a4)
+        bulk_g2s(sl + 68 * a4 + (full ? 0 : 2), src4[a4] + g - (full ? 2 : 0), wb, bar);
+      bulk_g2s(sl + 272, c.x + g, 512, bar);
+      bulk_g2s(sl + 336, c.ds + g, 512, bar);
+      int32_t* si = reinterpret_cast<int32_t*>(sl + 400);
+      for (int k = 0; k < 4; ++k) bulk_g2s(si + k * 64, C.ecol + k * es + b, 256, bar);
     }
-    // halo: rows b-2, b-1 and b+64, b+65 of r, q, p, D^-1 (chain neighbours across the edge)
-    if (lane < 8 && (lane >= 4 || b >= 2)) {
-      const int a4 = lane & 3;
-      const double* src = a4 == 0 ? c.rs : a4 == 1 ? c.qs : a4 == 2 ? c.ps : c.P->dinv;
-      cp16(sl + 512 + 4 * a4 + 2 * (lane >> 2), src + off + (lane < 4 ? b - 2 : b + 64));
-    }
-    cp_commit();
   };
-#pragma unroll
-  for (int d = 0; d < kStages - 1; ++d) {
-    if (wg + d * W < nch) prefetch(wg + d * W);
-    else cp_commit();
-  }
+  if (wg >= nch) return;
+  prefetch(wg);
+  if (wg + W < nch) prefetch(wg + W);
+  st.wait(tix(wg));
+  FarG fcur = far_gather(c, slot(wg), lane, off + 64 * (int64_t)wg + 2 * lane);
   for (int m = wg; m < nch; m += W) {
-    if (m + (kStages - 1) * W < nch) prefetch(m + (kStages - 1) * W);
-    else cp_commit();
-    cp_wait<kStages - 1>();
-    const double* sl = wsm + ((m / W) % kStages) * kSlotE;
-    const int32_t* si = reinterpret_cast<const int32_t*>(sl + 6 * 64);
+    if (m + 2 * W < nch) prefetch(m + 2 * W);                    // stage A
+    FarG fnxt;
+    fnxt.s0 = fnxt.s1 = -1;
+    fnxt.more = 0;
+    fnxt.r0 = fnxt.q0 = fnxt.p0 = fnxt.d0 = fnxt.r1 = fnxt.q1 = fnxt.p1 = fnxt.d1 = 0.0;
+    if (m + W < nch) {                                            // stage B
+      st.wait(tix(m + W));
+      fnxt = far_gather(c, slot(m + W), lane, off + 64 * (int64_t)(m + W) + 2 * lane);
+    }
+    // stage C: chunk m
+    const double* sl = slot(m);
     const int base = 64 * m + 2 * lane;
-    double pc[2], rc[2], dc[2], dsv[2];
-    int32_t j[2][4];
+    const int64_t g = off + base;
+    const bool ok0 = base < r1, ok1 = base + 1 < r1;
+    double pc[2], rc[2], dc[2];
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
-      const int l2 = 2 * lane + h;
-      const double ro = sl[0 * 64 + l2], qo = sl[1 * 64 + l2], po = sl[2 * 64 + l2];
-      dc[h] = sl[3 * 64 + l2];
-      rc[h] = __fma_rn(-c.a, qo, ro);
-      pc[h] = __fma_rn(dc[h], rc[h], __dmul_rn(c.b, po));
-      dsv[h] = sl[5 * 64 + l2];
-#pragma unroll
-      for (int k = 0; k < 4; ++k) j[h][k] = si[k * 64 + l2];
+      const int w = 2 + 2 * lane + h;
+      rc[h] = __fma_rn(-c.a, sl[68 + w], sl[w]);
+      dc[h] = sl[204 + w];
+      pc[h] = __fma_rn(dc[h], rc[h], __dmul_rn(c.b, sl[136 + w]));
     }
-    const bool ok0 = base < r1, ok1 = base + 1 < r1;
-    const int64_t g = off + base;
+    __syncwarp();                                                 // previous chunk's pnb reads done
+    pnb[2 + 2 * lane] = pc[0];
+    pnb[3 + 2 * lane] = pc[1];
+    if (lane < 4) {                                               // halo rows 0, 1, 66, 67
+      const int w = lane < 2 ? lane : 64 + lane;
+      pnb[w] = pnew(sl[w], sl[68 + w], sl[136 + w], sl[204 + w], c.a, c.b);
+    }
     {
-      const double2 xo = *reinterpret_cast<const double2*>(sl + 4 * 64 + 2 * lane);
-      const double2 po = *reinterpret_cast<const double2*>(sl + 2 * 64 + 2 * lane);
-      const double2 xn = make_double2(__fma_rn(c.a, po.x, xo.x), __fma_rn(c.a, po.y, xo.y));
+      const double2 xo = *reinterpret_cast<const double2*>(sl + 272 + 2 * lane);
+      const double po0 = sl[136 + 2 + 2 * lane], po1 = sl[136 + 3 + 2 * lane];
+      const double2 xn = make_double2(__fma_rn(c.a, po0, xo.x), __fma_rn(c.a, po1, xo.y));
       if (ok1) {
         *reinterpret_cast<double2*>(c.x + g) = xn;
         st2mut(c.rd + g, make_double2(rc[0], rc[1]));
@@ -487,99 +649,46 @@ __device__ void iter_ells(const Ctx& c, const ContDev& C, int wg, int W, double*
         stmut(c.pd + g, pc[0]);
       }
     }
-    // neighbours inside this 64-row chunk come from the staged copy in shared memory;
-    // the others are gathered from global memory, branch-free: an absent neighbour (-1)
-    // reads the zero slack element at index N (always L1-hot) and is discarded.
-    // Neighbours inside the chunk or its 2-row halo come from the staged copy in shared
-    // memory.  The rest ("far": junction links of the chain numbering) are gathered from
-    // global memory, at most two per lane in one batch; a warp with no far neighbour
-    // issues no gather at all.
-    const int64_t cb = off + 64 * (int64_t)m;
-    double pj[2][4];
-    int64_t fidx[2] = {g, g};
-    int fslot[2] = {-1, -1};
-    int nfar = 0;
-#pragma unroll
-    for (int h = 0; h < 2; ++h)
-#pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        const int64_t jj = j[h][k];
-        const int64_t li = jj - cb;
-        const bool in = jj >= 0 && li >= -2 && li < 66;       // chunk or its 2-row halo
-        double rr_, qq_, pp_, dd_;
-        if (in && li >= 0 && li < 64) {
-          const int l = (int)li;
-          rr_ = sl[l];
-          qq_ = sl[64 + l];
-          pp_ = sl[128 + l];
-          dd_ = sl[192 + l];
-        } else {
-          const int hh = in ? (li < 0 ? (int)li + 2 : (int)li - 62) : 0;
-          rr_ = sl[512 + hh];
-          qq_ = sl[516 + hh];
-          pp_ = sl[520 + hh];
-          dd_ = sl[524 + hh];
-        }
-        pj[h][k] = jj < 0 ? pc[h] : pnew(rr_, qq_, pp_, dd_, c.a, c.b);
-        if (jj >= 0 && !in) {
-          if (nfar < 2) {
-            fidx[nfar] = jj;
-            fslot[nfar] = 4 * h + k;
-          }
-          ++nfar;
-        }
-      }
-    const int wfar = __reduce_max_sync(0xffffffffu, (unsigned)nfar);
-    if (wfar > 0) {
-      const double v0 = c.pn_at(fidx[0]);
-      const double v1 = c.pn_at(fidx[1]);
-#pragma unroll
-      for (int h = 0; h < 2; ++h)
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          if (fslot[0] == 4 * h + k) pj[h][k] = v0;
-          if (fslot[1] == 4 * h + k) pj[h][k] = v1;
-        }
-      if (wfar > 2) {                                         // rare: > 2 far neighbours in a lane
-#pragma unroll
-        for (int h = 0; h < 2; ++h)
-#pragma unroll
-          for (int k = 0; k < 4; ++k) {
-            const int64_t jj = j[h][k];
-            const int64_t li = jj - cb;
-            const bool far = jj >= 0 && !(li >= -2 && li < 66);
-            if (far && fslot[0] != 4 * h + k && fslot[1] != 4 * h + k) pj[h][k] = c.pn_at(jj);
-          }
-      }
-    }
+    int32_t j[2][4];
+    ell_codes(sl, lane, j);
+    __syncwarp();
     double qv[2];
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
       double s = 0.0;
 #pragma unroll
-      for (int k = 0; k < 4; ++k) s += pc[h] - pj[h][k];
-      qv[h] = dsv[h] * pc[h] + C.Tconst * s;
+      for (int k = 0; k < 4; ++k) {
+        const int32_t cd = j[h][k];
+        double v = pc[h];                                          // -1: no neighbour
+        if (cd <= -2) v = pnb[-2 - cd];
+        else if (cd >= 0) {
+          if (fcur.s0 == 4 * h + k) v = fcur.v0(c);
+          else if (fcur.s1 == 4 * h + k) v = fcur.v1(c);
+          else v = c.pn_at(cd);                                    // rare: > 2 far in this lane
+        }
+        s += pc[h] - v;
+      }
+      qv[h] = sl[336 + 2 * lane + h] * pc[h] + C.Tconst * s;
       if (CPL && base + h < r1) qv[h] += c.couple_q(g + h, pc[h]);
     }
     if (ok1) st2mut(c.qd + g, make_double2(qv[0], qv[1]));
     else if (ok0) stmut(c.qd + g, qv[0]);
     if (ok0) c.accum(acc, pc[0], rc[0], dc[0], qv[0]);
     if (ok1) c.accum(acc, pc[1], rc[1], dc[1], qv[1]);
+    fcur = fnxt;
   }
-  cp_wait<0>();
 }
 
-// Resident variant of iter_ells for latency-bound graphs (every warp owns <= kStages
-// chunks): the chunks' r, q, p, x, D^-1, shift and ELL columns live in
-// this warp's shared-memory slots for the whole solve, so an iteration reads no
-// streamed operand from memory; in-chunk neighbours read the new p_j straight from
-// shared memory; only neighbours owned by other warps are gathered (from the previous
-// iteration's r, q, p in global memory, recomputed with pnew as everywhere else).
-// r, p, q are still stored to global every iteration for those gathers; x is flushed
-// at the end of the solve (flush_ells_res).
+// Resident variant for latency-bound graphs (every warp owns <= kStages chunks,
+// DESIGN.md §5.3): the chunks' r, q, p, x, D^-1, shift and codes stay in this warp's
+// slots for the whole solve, so an iteration streams nothing; in-chunk neighbours read
+// the new p straight from the slot; halo and far neighbours (owned by other warps) are
+// gathered from the previous iteration's r, q, p in global memory.  r, p, q are stored
+// to global every iteration for those gathers; x is flushed at the end of the solve.
 template <bool CPL>
-__device__ void iter_ells_res(const Ctx& c, const ContDev& C, int wg, int W, double* wsm, bool first,
+__device__ void iter_ells_res(const Ctx& c, const ContDev& C, int wg, int W, const Stage& st, bool first,
                               double (&acc)[kNPart]) {
+  double* wsm = st.wsm;
   const int lane = threadIdx.x & 31;
   const int64_t off = C.off, es = C.estride;
   const int r1 = (int)C.n;
@@ -587,46 +696,43 @@ __device__ void iter_ells_res(const Ctx& c, const ContDev& C, int wg, int W, dou
   if (first) {
     for (int m = wg, t = 0; m < nch; m += W, ++t) {
       double* sl = wsm + t * kSlotE;
-      const int64_t b = 64 * (int64_t)m, g = off + b + 2 * lane;
-      cp16(sl + 0 * 64 + 2 * lane, c.rs + g);
-      cp16(sl + 1 * 64 + 2 * lane, c.qs + g);
-      cp16(sl + 2 * 64 + 2 * lane, c.ps + g);
-      cp16(sl + 3 * 64 + 2 * lane, c.P->dinv + g);
-      cp16(sl + 4 * 64 + 2 * lane, c.x + g);
-      cp16(sl + 5 * 64 + 2 * lane, c.ds + g);
-      int32_t* si = reinterpret_cast<int32_t*>(sl + 6 * 64);
-#pragma unroll
-      for (int u2 = 0; u2 < 2; ++u2) {
-        const int u = lane + 32 * u2, k = u >> 4, part = u & 15;
-        cp16(si + k * 64 + 4 * part, C.ecol + k * es + b + 4 * part);
+      __syncwarp();
+      if (lane == 0) {
+        const int64_t b = 64 * (int64_t)m, g = off + b;
+        st.begin(t, 6u * 512u + 4u * 256u);
+        uint64_t* bar = st.bars + t;
+        bulk_g2s(sl + 2, c.rs + g, 512, bar);
+        bulk_g2s(sl + 68 + 2, c.qs + g, 512, bar);
+        bulk_g2s(sl + 136 + 2, c.ps + g, 512, bar);
+        bulk_g2s(sl + 204 + 2, c.P->dinv + g, 512, bar);
+        bulk_g2s(sl + 272, c.x + g, 512, bar);
+        bulk_g2s(sl + 336, c.ds + g, 512, bar);
+        int32_t* si = reinterpret_cast<int32_t*>(sl + 400);
+        for (int k = 0; k < 4; ++k) bulk_g2s(si + k * 64, C.ecol + k * es + b, 256, bar);
       }
     }
-    cp_commit();
-    cp_wait<0>();
-    __syncwarp();
+    for (int m = wg, t = 0; m < nch; m += W, ++t) st.wait(t);
   }
   for (int m = wg, t = 0; m < nch; m += W, ++t) {
     double* sl = wsm + t * kSlotE;
-    const int32_t* si = reinterpret_cast<const int32_t*>(sl + 6 * 64);
     const int base = 64 * m + 2 * lane;
     const int64_t g = off + base;
     const int64_t cb = off + 64 * (int64_t)m;
     const bool ok0 = base < r1, ok1 = base + 1 < r1;
-    double pc[2], rc[2], dc[2], dsv[2];
+    double pc[2], rc[2], dc[2], po[2];
     int32_t j[2][4];
+    ell_codes(sl, lane, j);
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
-      const int l2 = 2 * lane + h;
-      const double ro = sl[l2], qo = sl[64 + l2], po = sl[128 + l2];
-      dc[h] = sl[192 + l2];
-      rc[h] = __fma_rn(-c.a, qo, ro);
-      pc[h] = __fma_rn(dc[h], rc[h], __dmul_rn(c.b, po));
-      dsv[h] = sl[320 + l2];
-      sl[256 + l2] = __fma_rn(c.a, po, sl[256 + l2]);           // x (flushed at the end)
-#pragma unroll
-      for (int k = 0; k < 4; ++k) j[h][k] = si[k * 64 + l2];
+      const int w = 2 + 2 * lane + h;
+      po[h] = sl[136 + w];
+      rc[h] = __fma_rn(-c.a, sl[68 + w], sl[w]);
+      dc[h] = sl[204 + w];
+      pc[h] = __fma_rn(dc[h], rc[h], __dmul_rn(c.b, po[h]));
+      sl[272 + 2 * lane + h] = __fma_rn(c.a, po[h], sl[272 + 2 * lane + h]);   // x
     }
-    // far neighbours: issue the gathers first (previous iteration's r, q, p in global)
+    // neighbours outside the chunk (halo window slots and far): previous iteration's
+    // values from global memory, at most 2 per lane per batch
     int64_t fidx[2] = {g, g};
     int fslot[2] = {-1, -1};
     int nfar = 0;
@@ -634,9 +740,11 @@ __device__ void iter_ells_res(const Ctx& c, const ContDev& C, int wg, int W, dou
     for (int h = 0; h < 2; ++h)
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
-        const int64_t jj = j[h][k];
-        const int64_t li = jj - cb;
-        if (jj >= 0 && !(li >= 0 && li < 64)) {
+        const int32_t cd = j[h][k];
+        const int w = -2 - cd;
+        const bool out = cd >= 0 || (cd <= -2 && (w < 2 || w >= 66));
+        if (out) {
+          const int64_t jj = cd >= 0 ? (int64_t)cd : cb + w - 2;
           if (nfar < 2) {
             fidx[nfar] = jj;
             fslot[nfar] = 4 * h + k;
@@ -644,18 +752,23 @@ __device__ void iter_ells_res(const Ctx& c, const ContDev& C, int wg, int W, dou
           ++nfar;
         }
       }
-    const int wfar = __reduce_max_sync(0xffffffffu, (unsigned)nfar);
-    double v0 = 0.0, v1 = 0.0;
-    if (wfar > 0) {
-      v0 = c.pn_at(fidx[0]);
-      v1 = c.pn_at(fidx[1]);
+    const unsigned wfar = __reduce_max_sync(0xffffffffu, (unsigned)nfar);
+    double fr0 = 0.0, fq0 = 0.0, fp0 = 0.0, fd0 = 0.0, fr1 = 0.0, fq1 = 0.0, fp1 = 0.0, fd1 = 0.0;
+    if (wfar > 0) {              // raw loads now, p_j later: the trip overlaps the publishing
+      fr0 = ldnb(c.rs + fidx[0]);
+      fq0 = ldnb(c.qs + fidx[0]);
+      fp0 = ldnb(c.ps + fidx[0]);
+      fd0 = ldro(c.P->dinv + fidx[0]);
+      fr1 = ldnb(c.rs + fidx[1]);
+      fq1 = ldnb(c.qs + fidx[1]);
+      fp1 = ldnb(c.ps + fidx[1]);
+      fd1 = ldro(c.P->dinv + fidx[1]);
     }
-    // publish: own r_j, p_j into the slots (p_j is what in-chunk neighbours need)
     __syncwarp();
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
-      sl[2 * lane + h] = rc[h];
-      sl[128 + 2 * lane + h] = pc[h];
+      sl[2 + 2 * lane + h] = rc[h];
+      sl[136 + 2 + 2 * lane + h] = pc[h];
     }
     if (ok1) {
       st2mut(c.rd + g, make_double2(rc[0], rc[1]));
@@ -665,40 +778,26 @@ __device__ void iter_ells_res(const Ctx& c, const ContDev& C, int wg, int W, dou
       stmut(c.pd + g, pc[0]);
     }
     __syncwarp();
-    double pj[2][4];
-#pragma unroll
-    for (int h = 0; h < 2; ++h)
-#pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        const int64_t jj = j[h][k];
-        const int64_t li = jj - cb;
-        const bool in = jj >= 0 && li >= 0 && li < 64;
-        double v = in ? sl[128 + (int)li] : pc[h];
-        if (fslot[0] == 4 * h + k) v = v0;
-        else if (fslot[1] == 4 * h + k) v = v1;
-        pj[h][k] = v;
-      }
-    if (wfar > 2) {
-#pragma unroll
-      for (int h = 0; h < 2; ++h)
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          const int64_t jj = j[h][k];
-          const int64_t li = jj - cb;
-          if (jj >= 0 && !(li >= 0 && li < 64) && fslot[0] != 4 * h + k && fslot[1] != 4 * h + k)
-            pj[h][k] = c.pn_at(jj);
-        }
-    }
     double qv[2];
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
       double s = 0.0;
 #pragma unroll
-      for (int k = 0; k < 4; ++k) s += pc[h] - pj[h][k];
-      qv[h] = dsv[h] * pc[h] + C.Tconst * s;
+      for (int k = 0; k < 4; ++k) {
+        const int32_t cd = j[h][k];
+        const int w = -2 - cd;
+        double v = pc[h];
+        if (fslot[0] == 4 * h + k) v = pnew(fr0, fq0, fp0, fd0, c.a, c.b);
+        else if (fslot[1] == 4 * h + k) v = pnew(fr1, fq1, fp1, fd1, c.a, c.b);
+        else if (cd <= -2 && w >= 2 && w < 66) v = sl[136 + w];
+        else if (cd >= 0) v = c.pn_at(cd);                               // rare: > 2 outside
+        else if (cd <= -2) v = c.pn_at(cb + w - 2);
+        s += pc[h] - v;
+      }
+      qv[h] = sl[336 + 2 * lane + h] * pc[h] + C.Tconst * s;
     }
-    sl[64 + 2 * lane] = qv[0];
-    sl[64 + 2 * lane + 1] = qv[1];
+    sl[68 + 2 + 2 * lane] = qv[0];
+    sl[68 + 3 + 2 * lane] = qv[1];
     if (ok1) st2mut(c.qd + g, make_double2(qv[0], qv[1]));
     else if (ok0) stmut(c.qd + g, qv[0]);
     if (ok0) c.accum(acc, pc[0], rc[0], dc[0], qv[0]);
@@ -713,44 +812,8 @@ __device__ void flush_ells_res(const ContDev& C, int wg, int W, const double* ws
     const double* sl = wsm + t * kSlotE;
     for (int h = 0; h < 2; ++h) {
       const int64_t i = 64 * (int64_t)m + 2 * lane + h;
-      if (i < C.n) x[C.off + i] = sl[256 + 2 * lane + h];
+      if (i < C.n) x[C.off + i] = sl[272 + 2 * lane + h];
     }
-  }
-}
-
-// ---------------------------------------------------------------- CG pass, graph rows, ELL
-// lane-per-row over a k-major ELL copy of the adjacency (width W, -1 = no entry): the W
-// column indices arrive in one coalesced trip, then all neighbour gathers in one more.
-template <bool CPL, int W>
-__device__ void iter_ell(const Ctx& c, const ContDev& C, int r0, int r1, double (&acc)[kNPart]) {
-  const int lane = threadIdx.x & 31;
-  const int64_t n = C.n;
-  for (int i = r0 + lane; i < r1; i += 32) {
-    const int64_t gi = C.off + i;
-    int32_t j[W];
-#pragma unroll
-    for (int k = 0; k < W; ++k) j[k] = ldro(C.ecol + k * n + i);
-    double pc, rc, dc;
-    c.own(gi, pc, rc, dc);
-    double pj[W];
-#pragma unroll
-    for (int k = 0; k < W; ++k) {
-      const double v = c.pn_at(j[k] >= 0 ? (int64_t)j[k] : gi);   // branch-free gather
-      pj[k] = (j[k] >= 0) ? v : pc;
-    }
-    double s = 0.0;
-    if (C.val) {
-#pragma unroll
-      for (int k = 0; k < W; ++k) s += (j[k] >= 0 ? ldro(C.val + k * n + i) : 0.0) * (pc - pj[k]);
-    } else {
-#pragma unroll
-      for (int k = 0; k < W; ++k) s += pc - pj[k];
-      s *= C.Tconst;
-    }
-    double qv = ldro(c.ds + gi) * pc + s;
-    if (CPL) qv += c.couple_q(gi, pc);
-    stmut(c.qd + gi, qv);
-    c.accum(acc, pc, rc, dc, qv);
   }
 }
 
@@ -963,7 +1026,12 @@ __device__ void run_group(const StepParams& P, int g, int cl, double* x, const d
   const bool leader = (cl == 0 && threadIdx.x == 0);
   long long t0 = leader ? globaltimer() : 0;
   extern __shared__ __align__(16) double dsm[];
-  double* wsm = dsm + (threadIdx.x >> 5) * kWarpSmem;      // this warp's staging slots
+  const int wid = threadIdx.x >> 5;
+  Stage st;
+  st.wsm = dsm + wid * kWarpSmem;                            // this warp's staging slots
+  st.bars = reinterpret_cast<uint64_t*>(dsm + kWarps * kWarpSmem) + wid * kNBars;
+  st.ph = reinterpret_cast<unsigned*>(dsm + kWarps * kWarpSmem + kWarps * kNBars) + 2 * wid;
+  double* wsm = st.wsm;
 
   double a3[3] = {0.0, 0.0, 0.0};
   for (int k = 0; k < P.L; ++k)
@@ -1009,17 +1077,15 @@ __device__ void run_group(const StepParams& P, int g, int cl, double* x, const d
       double a5[kNPart] = {0.0, 0.0, 0.0, 0.0, 0.0};
       for (int k = 0; k < P.L; ++k)
         if (((G.cont_mask >> k) & 1) && P.cont[k].rr) {
-          if (P.cont[k].resident) iter_ells_res<CPL>(c, P.cont[k], wg, W, wsm, j == 0, a5);
-          else iter_ells<CPL>(c, P.cont[k], wg, W, wsm, a5);
+          if (P.cont[k].resident) iter_ells_res<CPL>(c, P.cont[k], wg, W, st, j == 0, a5);
+          else iter_ells<CPL>(c, P.cont[k], wg, W, st, a5);
         }
       for (int it = ib + wg; it < ie; it += W) {
         const Item item = (it == ib + wg) ? it0 : P.items[it];
         const ContDev& C = P.cont[item.cont];
         if (item.kind == ITEM_GRID) {
-          if (item.w == 64) iter_grid2s<CPL>(c, C, item.a, item.b, item.c, wsm, a5);
+          if (item.w == 64) iter_grid2s<CPL>(c, C, item.a, item.b, item.c, st, a5);
           else iter_grid<CPL>(c, C, item.a, item.b, item.c, a5);
-        } else if (C.ecol) {
-          iter_ell<CPL, 4>(c, C, item.a, item.b, a5);
         } else if (C.lpr == 8) {
           iter_graph8<CPL>(c, C, item.a, item.b, a5);
         } else {
@@ -1085,6 +1151,17 @@ __device__ __forceinline__ void grid_barrier(const StepParams& P, unsigned long 
 }
 
 __global__ void __launch_bounds__(kThreads, kMinBlocks) step_kernel(const __grid_constant__ StepParams P) {
+  {  // staging barriers: one mbarrier per slot per warp (arrival count 1: the issuing lane)
+    extern __shared__ __align__(16) double dsm[];
+    if ((threadIdx.x & 31) == 0) {
+      const int wid = threadIdx.x >> 5;
+      uint64_t* bars = reinterpret_cast<uint64_t*>(dsm + kWarps * kWarpSmem) + wid * kNBars;
+      for (int t = 0; t < kNBars; ++t) mbar_init(bars + t, 1);
+      *(reinterpret_cast<unsigned*>(dsm + kWarps * kWarpSmem + kWarps * kNBars) + 2 * wid) = 0u;
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+  }
   const int failed = *(volatile const int32_t*)P.fail;
   const int cur = *(volatile const int32_t*)P.cur;
   if (!failed) {
