@@ -27,7 +27,7 @@ constexpr int kSlack = 128;            // extra doubles after every per-DOF arra
 // cp.async staging: per warp, two slots of the next rows' operands
 constexpr int kSlotG = 536;            // grid strip slot: 8 arrays x 64 doubles + 18 edge doubles
 constexpr int kSlotE = 528;            // ELL chunk slot: r, q, p, D^-1 windows (68), x, shift (64), 4 x 64 int32 codes
-constexpr int kStagesE = 3;                // ELL pass: load -> gather -> compute pipeline
+constexpr int kStagesE = 2;                // ELL pass: chunk in flight + chunk computed
 constexpr int kPnBuf = 72;                 // ELL pass: new p of the chunk window (68) per warp
 constexpr int kWarpSmem = ((kStages * kSlotG > kStagesE * kSlotE) ? kStages * kSlotG : kStagesE * kSlotE) + kPnBuf;
 // bytes per CTA: staging slots, then one mbarrier per slot per warp, then a parity word per warp

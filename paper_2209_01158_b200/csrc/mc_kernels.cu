@@ -504,23 +504,21 @@ __device__ void iter_grid2s(const Ctx& c, const ContDev& C, int x0, int y0, int 
 }
 
 // ELL rows in 64-row chunks swept round-robin by the group's warps (lane l owns rows
-// 2l, 2l+1 of a chunk); three-stage software pipeline per warp:
-//   A  TMA bulk copies of chunk m+2W: r, q, p, D^-1 over the chunk and a 2-row halo on
-//      each side (68-row window), x, shift, and the 4 ELL codes;
-//   B  for chunk m+W (landed): gather the "far" neighbours (code >= 0: neither in the
-//      chunk nor in its halo, at most 2 per lane per batch) — their p_j recomputed from
-//      the previous iteration's r, q, p, stable for the whole pass;
-//   C  chunk m: new p of every window row into a per-warp buffer, then q from it.
+// 2l, 2l+1 of a chunk).  Per chunk: TMA bulk copies of the NEXT chunk's r, q, p, D^-1
+// over the chunk and a 2-row halo on each side (68-row window), x, shift and the 4 ELL
+// codes are issued; this chunk's "far" neighbours (code >= 0: neither in the chunk nor
+// its halo, at most 2 per lane per batch) are gathered, p_j recomputed from the previous
+// iteration's r, q, p; the new p of every window row goes to a per-warp buffer and q is
+// formed from it.  (A three-stage load / gather / compute pipeline measured no faster.)
 // ELL codes are pre-classified on the host against the static chunk (mc_api.cu).
 // Neighbours in another chunk were (or are about to be) streamed by another warp of
 // the sweep, so the far gathers hit L2.
 struct FarG {
-  double r0, q0, p0, d0, r1, q1, p1, d1;   // raw previous-iteration values (consumed later,
-                                           // so the gather latency overlaps other work)
+  double w0, w1;   // p_j of the (at most 2) far neighbours of this lane
   int s0, s1;      // 4*h + k slot the value belongs to, -1 = none
   int more;        // warp-uniform: some lane has > 2 far neighbours in this chunk
-  __device__ __forceinline__ double v0(const Ctx& c) const { return pnew(r0, q0, p0, d0, c.a, c.b); }
-  __device__ __forceinline__ double v1(const Ctx& c) const { return pnew(r1, q1, p1, d1, c.a, c.b); }
+  __device__ __forceinline__ double v0(const Ctx&) const { return w0; }
+  __device__ __forceinline__ double v1(const Ctx&) const { return w1; }
 };
 
 __device__ __forceinline__ void ell_codes(const double* sl, int lane, int32_t (&j)[2][4]) {
@@ -554,17 +552,10 @@ __device__ __forceinline__ FarG far_gather(const Ctx& c, const double* sl, int l
       }
   const unsigned wfar = __reduce_max_sync(0xffffffffu, (unsigned)nfar);
   f.more = wfar > 2;
+  f.w0 = f.w1 = 0.0;
   if (wfar > 0) {
-    f.r0 = ldnb(c.rs + i0);
-    f.q0 = ldnb(c.qs + i0);
-    f.p0 = ldnb(c.ps + i0);
-    f.d0 = ldro(c.P->dinv + i0);
-    f.r1 = ldnb(c.rs + i1);
-    f.q1 = ldnb(c.qs + i1);
-    f.p1 = ldnb(c.ps + i1);
-    f.d1 = ldro(c.P->dinv + i1);
-  } else {
-    f.r0 = f.q0 = f.p0 = f.d0 = f.r1 = f.q1 = f.p1 = f.d1 = 0.0;
+    f.w0 = c.pn_at(i0);
+    f.w1 = c.pn_at(i1);
   }
   return f;
 }
@@ -591,30 +582,25 @@ __device__ void iter_ells(const Ctx& c, const ContDev& C, int wg, int W, const S
       const unsigned wb = full ? 544u : 528u;
       st.begin(t, 4u * wb + 2u * 512u + 4u * 256u);
       uint64_t* bar = st.bars + t;
-      const double* src4[4] = {c.rs, c.qs, c.ps, c.P->dinv};
-      for (int a4 = 0; a4 < 4; ++a4)
-        bulk_g2s(sl + 68 * a4 + (full ? 0 : 2), src4[a4] + g - (full ? 2 : 0), wb, bar);
+      const int64_t g0 = g - (full ? 2 : 0);
+      const int d0 = full ? 0 : 2;
+      bulk_g2s(sl + d0, c.rs + g0, wb, bar);
+      bulk_g2s(sl + 68 + d0, c.qs + g0, wb, bar);
+      bulk_g2s(sl + 136 + d0, c.ps + g0, wb, bar);
+      bulk_g2s(sl + 204 + d0, c.P->dinv + g0, wb, bar);
       bulk_g2s(sl + 272, c.x + g, 512, bar);
       bulk_g2s(sl + 336, c.ds + g, 512, bar);
       int32_t* si = reinterpret_cast<int32_t*>(sl + 400);
+#pragma unroll
       for (int k = 0; k < 4; ++k) bulk_g2s(si + k * 64, C.ecol + k * es + b, 256, bar);
     }
   };
   if (wg >= nch) return;
   prefetch(wg);
-  if (wg + W < nch) prefetch(wg + W);
-  st.wait(tix(wg));
-  FarG fcur = far_gather(c, slot(wg), lane, off + 64 * (int64_t)wg + 2 * lane);
   for (int m = wg; m < nch; m += W) {
-    if (m + 2 * W < nch) prefetch(m + 2 * W);                    // stage A
-    FarG fnxt;
-    fnxt.s0 = fnxt.s1 = -1;
-    fnxt.more = 0;
-    fnxt.r0 = fnxt.q0 = fnxt.p0 = fnxt.d0 = fnxt.r1 = fnxt.q1 = fnxt.p1 = fnxt.d1 = 0.0;
-    if (m + W < nch) {                                            // stage B
-      st.wait(tix(m + W));
-      fnxt = far_gather(c, slot(m + W), lane, off + 64 * (int64_t)(m + W) + 2 * lane);
-    }
+    if (m + W < nch) prefetch(m + W);                             // next chunk in flight
+    st.wait(tix(m));
+    const FarG fcur = far_gather(c, slot(m), lane, off + 64 * (int64_t)m + 2 * lane);
     // stage C: chunk m
     const double* sl = slot(m);
     const int base = 64 * m + 2 * lane;
@@ -675,7 +661,6 @@ __device__ void iter_ells(const Ctx& c, const ContDev& C, int wg, int W, const S
     else if (ok0) stmut(c.qd + g, qv[0]);
     if (ok0) c.accum(acc, pc[0], rc[0], dc[0], qv[0]);
     if (ok1) c.accum(acc, pc[1], rc[1], dc[1], qv[1]);
-    fcur = fnxt;
   }
 }
 
@@ -708,67 +693,79 @@ __device__ void iter_ells_res(const Ctx& c, const ContDev& C, int wg, int W, con
         bulk_g2s(sl + 272, c.x + g, 512, bar);
         bulk_g2s(sl + 336, c.ds + g, 512, bar);
         int32_t* si = reinterpret_cast<int32_t*>(sl + 400);
-        for (int k = 0; k < 4; ++k) bulk_g2s(si + k * 64, C.ecol + k * es + b, 256, bar);
+  #pragma unroll
+      for (int k = 0; k < 4; ++k) bulk_g2s(si + k * 64, C.ecol + k * es + b, 256, bar);
       }
     }
     for (int m = wg, t = 0; m < nch; m += W, ++t) st.wait(t);
+    // the slot is this warp's own copy: decode the ELL codes into global column
+    // indices once (-1 = none), so the loop below needs one compare per neighbour
+    for (int m = wg, t = 0; m < nch; m += W, ++t) {
+      int32_t* si = reinterpret_cast<int32_t*>(wsm + t * kSlotE + 400);
+      const int64_t cb = off + 64 * (int64_t)m;
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int e = lane + 32 * u, cd = si[e];
+        si[e] = cd <= -2 ? (int32_t)(cb + (-2 - cd) - 2) : cd;
+      }
+    }
+    __syncwarp();
   }
   for (int m = wg, t = 0; m < nch; m += W, ++t) {
     double* sl = wsm + t * kSlotE;
+    const int32_t* si = reinterpret_cast<const int32_t*>(sl + 400);
     const int base = 64 * m + 2 * lane;
     const int64_t g = off + base;
     const int64_t cb = off + 64 * (int64_t)m;
     const bool ok0 = base < r1, ok1 = base + 1 < r1;
-    double pc[2], rc[2], dc[2], po[2];
+    double pc[2], rc[2], dc[2], dsv[2];
     int32_t j[2][4];
-    ell_codes(sl, lane, j);
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
-      const int w = 2 + 2 * lane + h;
-      po[h] = sl[136 + w];
-      rc[h] = __fma_rn(-c.a, sl[68 + w], sl[w]);
-      dc[h] = sl[204 + w];
-      pc[h] = __fma_rn(dc[h], rc[h], __dmul_rn(c.b, po[h]));
-      sl[272 + 2 * lane + h] = __fma_rn(c.a, po[h], sl[272 + 2 * lane + h]);   // x
+      const int l2 = 2 * lane + h;
+      const double ro = sl[2 + l2], qo = sl[70 + l2], po = sl[138 + l2];
+      dc[h] = sl[206 + l2];
+      rc[h] = __fma_rn(-c.a, qo, ro);
+      pc[h] = __fma_rn(dc[h], rc[h], __dmul_rn(c.b, po));
+      dsv[h] = sl[336 + l2];
+      sl[272 + l2] = __fma_rn(c.a, po, sl[272 + l2]);           // x (flushed at the end)
+#pragma unroll
+      for (int k = 0; k < 4; ++k) j[h][k] = si[k * 64 + l2];
     }
-    // neighbours outside the chunk (halo window slots and far): previous iteration's
-    // values from global memory, at most 2 per lane per batch
-    int64_t fidx[2] = {g, g};
-    int fslot[2] = {-1, -1};
+    // neighbours outside the chunk: previous iteration's r, q, p from global memory
+    // (scalars, not arrays indexed by a runtime count: those would live in local memory)
+    int64_t fi0 = g, fi1 = g;
+    int fs0 = -1, fs1 = -1;
     int nfar = 0;
 #pragma unroll
     for (int h = 0; h < 2; ++h)
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
-        const int32_t cd = j[h][k];
-        const int w = -2 - cd;
-        const bool out = cd >= 0 || (cd <= -2 && (w < 2 || w >= 66));
-        if (out) {
-          const int64_t jj = cd >= 0 ? (int64_t)cd : cb + w - 2;
-          if (nfar < 2) {
-            fidx[nfar] = jj;
-            fslot[nfar] = 4 * h + k;
+        const int64_t jj = j[h][k];
+        const int64_t li = jj - cb;
+        if (jj >= 0 && !(li >= 0 && li < 64)) {
+          if (nfar == 0) {
+            fi0 = jj;
+            fs0 = 4 * h + k;
+          } else if (nfar == 1) {
+            fi1 = jj;
+            fs1 = 4 * h + k;
           }
           ++nfar;
         }
       }
-    const unsigned wfar = __reduce_max_sync(0xffffffffu, (unsigned)nfar);
-    double fr0 = 0.0, fq0 = 0.0, fp0 = 0.0, fd0 = 0.0, fr1 = 0.0, fq1 = 0.0, fp1 = 0.0, fd1 = 0.0;
-    if (wfar > 0) {              // raw loads now, p_j later: the trip overlaps the publishing
-      fr0 = ldnb(c.rs + fidx[0]);
-      fq0 = ldnb(c.qs + fidx[0]);
-      fp0 = ldnb(c.ps + fidx[0]);
-      fd0 = ldro(c.P->dinv + fidx[0]);
-      fr1 = ldnb(c.rs + fidx[1]);
-      fq1 = ldnb(c.qs + fidx[1]);
-      fp1 = ldnb(c.ps + fidx[1]);
-      fd1 = ldro(c.P->dinv + fidx[1]);
+    const int wfar = __reduce_max_sync(0xffffffffu, (unsigned)nfar);
+    double v0 = 0.0, v1 = 0.0;
+    if (wfar > 0) {
+      v0 = c.pn_at(fi0);
+      v1 = c.pn_at(fi1);
     }
+    // publish: own r_j, p_j into the slot (p_j is what in-chunk neighbours need)
     __syncwarp();
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
       sl[2 + 2 * lane + h] = rc[h];
-      sl[136 + 2 + 2 * lane + h] = pc[h];
+      sl[138 + 2 * lane + h] = pc[h];
     }
     if (ok1) {
       st2mut(c.rd + g, make_double2(rc[0], rc[1]));
@@ -778,26 +775,40 @@ __device__ void iter_ells_res(const Ctx& c, const ContDev& C, int wg, int W, con
       stmut(c.pd + g, pc[0]);
     }
     __syncwarp();
+    double pj[2][4];
+#pragma unroll
+    for (int h = 0; h < 2; ++h)
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const int64_t jj = j[h][k];
+        const int64_t li = jj - cb;
+        const bool in = jj >= 0 && li >= 0 && li < 64;
+        double v = in ? sl[138 + (int)li] : pc[h];
+        if (fs0 == 4 * h + k) v = v0;
+        else if (fs1 == 4 * h + k) v = v1;
+        pj[h][k] = v;
+      }
+    if (wfar > 2) {
+#pragma unroll
+      for (int h = 0; h < 2; ++h)
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const int64_t jj = j[h][k];
+          const int64_t li = jj - cb;
+          if (jj >= 0 && !(li >= 0 && li < 64) && fs0 != 4 * h + k && fs1 != 4 * h + k)
+            pj[h][k] = c.pn_at(jj);
+        }
+    }
     double qv[2];
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
       double s = 0.0;
 #pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        const int32_t cd = j[h][k];
-        const int w = -2 - cd;
-        double v = pc[h];
-        if (fslot[0] == 4 * h + k) v = pnew(fr0, fq0, fp0, fd0, c.a, c.b);
-        else if (fslot[1] == 4 * h + k) v = pnew(fr1, fq1, fp1, fd1, c.a, c.b);
-        else if (cd <= -2 && w >= 2 && w < 66) v = sl[136 + w];
-        else if (cd >= 0) v = c.pn_at(cd);                               // rare: > 2 outside
-        else if (cd <= -2) v = c.pn_at(cb + w - 2);
-        s += pc[h] - v;
-      }
-      qv[h] = sl[336 + 2 * lane + h] * pc[h] + C.Tconst * s;
+      for (int k = 0; k < 4; ++k) s += pc[h] - pj[h][k];
+      qv[h] = dsv[h] * pc[h] + C.Tconst * s;
     }
-    sl[68 + 2 + 2 * lane] = qv[0];
-    sl[68 + 3 + 2 * lane] = qv[1];
+    sl[70 + 2 * lane] = qv[0];
+    sl[70 + 2 * lane + 1] = qv[1];
     if (ok1) st2mut(c.qd + g, make_double2(qv[0], qv[1]));
     else if (ok0) stmut(c.qd + g, qv[0]);
     if (ok0) c.accum(acc, pc[0], rc[0], dc[0], qv[0]);
