@@ -44,7 +44,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", type=int, default=1)
-    ap.add_argument("--scheme", default="D", choices=["D", "coupled"])
+    ap.add_argument("--scheme", default="D", choices=["D", "coupled", "L", "U"])
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -57,6 +57,28 @@ def peaks():
         d = json.load(open(p))
         return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
     return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)"
+
+
+def ncu_traffic(cid, warmup):
+    """Mean DRAM bytes (read + write) per step_kernel launch from the committed ncu launch
+    list of this bench command (profiles/r01_launches_config{cid}.csv), warm-up launches
+    skipped; None when no such capture is committed."""
+    import csv
+    p = os.path.join(ROOT, "profiles", f"r01_launches_config{cid}.csv")
+    if not os.path.exists(p):
+        return None, None
+    rows = [r for r in csv.reader(l for l in open(p) if not l.startswith("=="))]
+    hdr = rows[0]
+    ik, im, iv = hdr.index("Kernel Name"), hdr.index("Metric Name"), hdr.index("Metric Value")
+    per = {}
+    for r in rows[1:]:
+        if "step_kernel" in r[ik] and r[im] in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+            per.setdefault(r[0], 0.0)
+            per[r[0]] += float(r[iv].replace(",", ""))
+    vals = [per[k] for k in sorted(per, key=int)][warmup:]
+    if not vals:
+        return None, None
+    return sum(vals) / len(vals), os.path.relpath(p, ROOT)
 
 
 def workload_name(cid, scheme):
@@ -149,15 +171,19 @@ class Clocks:
 
 
 # ------------------------------------------------------------------ distributed
-def dist_init(n):
+def dist_init(n, backend="nccl"):
+    """One process per GPU (torchrun env); replicas only."""
     if n <= 1 or "RANK" not in os.environ:
         return 0, 1, 0
     import torch.distributed as dist
     import torch
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     local = int(os.environ.get("LOCAL_RANK", rank))
-    torch.cuda.set_device(local)
-    dist.init_process_group("nccl", rank=rank, world_size=world, device_id=torch.device("cuda", local))
+    if backend == "nccl":
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", rank=rank, world_size=world, device_id=torch.device("cuda", local))
+    else:
+        dist.init_process_group(backend, rank=rank, world_size=world)
     return rank, world, local
 
 
@@ -172,9 +198,15 @@ def max_over_ranks(x, world):
         return x
     import torch
     import torch.distributed as dist
-    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dev = "cuda" if dist.get_backend() == "nccl" else "cpu"
+    t = torch.tensor([x], dtype=torch.float64, device=dev)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
+
+
+def aggregate(world, dof, steps, total_ms):
+    """Whole-job DOF-steps/s: every rank a replica of `dof` DOFs, time = max over ranks."""
+    return world * dof * steps / (total_ms * 1e-3)
 
 
 # ------------------------------------------------------------------ oracle legs (CPU)
@@ -185,7 +217,8 @@ def oracle_sample(scn, scheme, steps, budget_s=30.0):
     from oracle import assemble as asm, schemes
     t0 = time.perf_counter()
     sys_ = asm.assemble(scn)
-    st = schemes.make_stepper(sys_, "coupled" if scheme == "coupled" else "D", scn["T"] / scn["NT"])
+    order = list(range(sys_.L))          # continua ascend in permeability in every workload
+    st = schemes.make_stepper(sys_, scheme, scn["T"] / scn["NT"], order_by_k=order)
     setup = time.perf_counter() - t0
     u = sys_.u0.copy()
     done = 0
@@ -256,12 +289,13 @@ def main():
     clk = clocks.stop()
     step_ms = [a.elapsed_time(b) for a, b in ev]
     total_ms = max_over_ranks(sum(step_ms), world)
-    value = world * dof * args.steps / (total_ms * 1e-3)
+    value = aggregate(world, dof, args.steps, total_ms)
     # roofline of the dominant (only) kernel: the step kernel, one launch per step
     bytes_per = sum(step_bytes(pb, r, args.scheme) for r in reps) / args.steps
     kern_ms = sum(r["ms"] for r in reps) / args.steps
     peak, peak_src = peaks()
     achieved = bytes_per / (kern_ms * 1e-3) / 1e9
+    traffic, traffic_src = ncu_traffic(args.config, 3) if args.scheme == "D" else (None, None)
     # end to end through the C ABI with host buffers (pinned), copies inside the timed region
     e2e = None
     if not args.no_e2e:
@@ -290,10 +324,12 @@ def main():
                "sample": f"config{args.config} {args.scheme}-scheme, {done} oracle steps (SuperLU back-solves "
                          f"+ long-double flux refinement, 1 thread); assembly+factorisation {setup:.1f}s excluded"}
     its = [r["iters"] for r in reps]
+    # metric name follows the scheme actually timed
     mean_its = [sum(x[a] for x in its) / len(its) for a in range(len(its[0]))]
     if rank == 0:
         line = {
-            "metric": "fine-grid DOF-steps/s (decoupled, fp64)", "value": value, "unit": "DOF-steps/s",
+            "metric": "fine-grid DOF-steps/s (decoupled, fp64)" if args.scheme == "D" else
+                      f"fine-grid DOF-steps/s ({args.scheme}-scheme, fp64)", "value": value, "unit": "DOF-steps/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": total_ms / args.steps, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
@@ -304,7 +340,8 @@ def main():
                        "l2": "flushed between timed steps (256 MiB memset)",
                        "parallelism": f"replicas x{world}"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": None, "peak_source": peak_src,
+                         "frac": achieved / peak, "traffic": traffic, "traffic_source": traffic_src,
+                         "peak_source": peak_src,
                          "kernel": "mc::step_kernel", "bytes_per_launch": bytes_per,
                          "ms_per_launch": kern_ms},
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": args.steps, "clocks": clk,

@@ -64,7 +64,12 @@ typedef enum {
 
 typedef enum {
   MC_COUPLED = 0,      /* Eq. ct-mc: one CG solve over all continua per step            */
-  MC_DECOUPLED_D = 1   /* Eq. si-mc, D-scheme: one CG solve per continuum per step      */
+  MC_DECOUPLED_D = 1,  /* Eq. si-mc, D-scheme: one CG solve per continuum per step      */
+  MC_DECOUPLED_L = 2,  /* L-scheme: continua solved in ascending permeability, each
+                          taking the transfer from continua already solved at layer n
+                          (block lower-triangular A0)                 */
+  MC_DECOUPLED_U = 3   /* U-scheme: descending permeability (block upper-triangular A0,
+                          PAPER.md:562-580); needs mc_set_permeability_order            */
 } mc_scheme;
 
 typedef struct {
@@ -163,6 +168,13 @@ mc_status mc_set_continuum(mc_ctx* ctx, int32_t alpha, const mc_continuum_desc* 
 
 /* Add a transfer Q_ab.  All continua must be set first (else MC_ERR_STATE). */
 mc_status mc_set_coupling(mc_ctx* ctx, const mc_coupling_desc* desc);
+
+/* Order of the continua by ascending permeability k_1 < k_2 < ...:
+ * order[0] is the least permeable.  Required before MC_DECOUPLED_L / MC_DECOUPLED_U. */
+mc_status mc_set_permeability_order(mc_ctx* ctx, const int32_t* order);
+
+/* Advance one time layer by `scheme` (any mc_scheme). */
+mc_status mc_step(mc_ctx* ctx, int32_t scheme, mc_step_report* rep);
 
 /* Advance one time layer by the D-scheme / the coupled scheme.  Blocks until the step
  * completed; fills *rep (may be NULL).  On MC_ERR_NOCONV / MC_ERR_BREAKDOWN the state is

@@ -2,6 +2,7 @@
 
 TEST INFRASTRUCTURE ONLY (see oracle/__init__.py).
 
+L, U      the sequential schemes of PAPER.md:541-580 (SeqScheme).
 coupled   Eq. ct-mc:  M (p^n - p^{n-1})/tau + A p^n = F
           =>  (M/tau + A) p^n = M/tau p^{n-1} + F.
 D-scheme  Eq. si-mc with the D-split:
@@ -127,17 +128,54 @@ class DScheme:
         return out
 
 
-def make_stepper(sys: System, scheme: str, tau: float, method="splu", refine=True):
+class SeqScheme(DScheme):
+    """L- / U-scheme: Eq. si-mc with A0 block lower- (L) or upper- (U)
+    triangular once the continua are sorted by permeability k_1 < ... < k_L.  Written as
+    what the triangular A0 means: the continua are solved one after another — L in
+    ascending permeability, U in descending — and each solve takes the transfer from the
+    continua already solved in this step at layer n, from the others at layer n-1:
+
+        (M_a/tau + D_a + sum_b Q_ab) p_a^n = M_a/tau p_a^{n-1} + F_a
+                                             + sum_{b before a} Q_ab p_b^n + sum_{b after a} Q_ab p_b^{n-1}
+
+    `order_by_k` lists the continuum ids by ascending permeability."""
+
+    def __init__(self, sys: System, tau: float, order_by_k, kind="U", method="splu", refine=True):
+        super().__init__(sys, tau, method, refine)
+        order = list(order_by_k)
+        assert sorted(order) == list(range(sys.L))
+        self.order = order if kind == "L" else order[::-1]
+
+    def step(self, u):
+        A = sp.csr_matrix(self.sys.A)
+        new = u.copy()                      # continua solved so far hold layer n
+        for a in self.order:
+            s = self.sys.block(a)
+            b = self.sys.M[s] / self.tau * u[s] + self.sys.F[s]
+            for c in range(self.sys.L):
+                if c != a:                  # -A_ac = Q_ac: layer n if c already solved
+                    sc = self.sys.block(c)
+                    b = b - A[s, sc] @ new[sc]
+            new[s] = self.solvers[a].solve(b, u[s])
+        return new
+
+
+def make_stepper(sys: System, scheme: str, tau: float, method="splu", refine=True, order_by_k=None):
     if scheme == "coupled":
         return Coupled(sys, tau, method, refine)
     if scheme in ("D", "decoupled", "d"):
         return DScheme(sys, tau, method, refine)
+    if scheme in ("L", "U"):
+        if order_by_k is None:
+            raise ValueError("L/U schemes need the continua ordered by permeability")
+        return SeqScheme(sys, tau, order_by_k, scheme, method, refine)
     raise ValueError(scheme)
 
 
-def run(sys: System, scheme: str, tau: float, n_steps: int, method="splu", u0=None, refine=True):
+def run(sys: System, scheme: str, tau: float, n_steps: int, method="splu", u0=None, refine=True,
+        order_by_k=None):
     """Trajectory [p^1, ..., p^n_steps] (full concatenated vectors)."""
-    st = make_stepper(sys, scheme, tau, method, refine)
+    st = make_stepper(sys, scheme, tau, method, refine, order_by_k)
     u = sys.u0.copy() if u0 is None else np.asarray(u0, dtype=np.float64).copy()
     out = []
     for _ in range(n_steps):

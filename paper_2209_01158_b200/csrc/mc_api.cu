@@ -95,7 +95,9 @@ struct mc_ctx {
   int32_t cur_host = 0;
   int32_t step_no = 0;
   int64_t last_iters[MC_MAX_CONTINUA] = {0};
-  Plan plan[2];                                 // by scheme
+  Plan plan[4];                                 // by scheme
+  int32_t korder[MC_MAX_CONTINUA] = {0};        // continua by ascending permeability
+  bool has_korder = false;
   int uploaded_plan = -1;                       // scheme whose items are on device
   std::vector<void*> allocs;
 };
@@ -855,6 +857,27 @@ static Plan make_plan(const mc_ctx* c, int scheme) {
   }
   const int L = c->L;
   P.ngroups = L;
+  if (scheme == MC_DECOUPLED_L || scheme == MC_DECOUPLED_U) {
+    // sequential: one phase per continuum in permeability order, all CTAs each
+    P.nphases = L;
+    for (int pos = 0; pos < L; ++pos) {
+      const int a = scheme == MC_DECOUPLED_L ? c->korder[pos] : c->korder[L - 1 - pos];
+      Group& g = P.grp[a];
+      g.phase = pos;
+      g.cta_begin = 0;
+      g.cta_count = T;
+      g.tol2 = c->hc[a].rtol * c->hc[a].rtol;
+      g.maxit = default_maxit(c, c->hc[a].n);
+      g.cont_mask = 1 << a;
+    }
+    for (int a = 0; a < L; ++a) {
+      P.grp[a].item_begin = (int32_t)P.items.size();
+      add_items(c, a, T * kWarps, P.items);
+      P.grp[a].item_count = (int32_t)P.items.size() - P.grp[a].item_begin;
+    }
+    P.valid = true;
+    return P;
+  }
   bool all_large = true, hist = true;
   for (int a = 0; a < L; ++a) {
     if (c->hc[a].n < kLargeRows) all_large = false;
@@ -997,6 +1020,7 @@ static mc_status enqueue_step(mc_ctx* c, int scheme) {
   P.ngroups = cp.ngroups;
   P.nphases = cp.nphases;
   P.coupled = (scheme == MC_COUPLED);
+  P.gs = (scheme == MC_DECOUPLED_L || scheme == MC_DECOUPLED_U) ? 1 : 0;
   P.total_ctas = c->total_ctas;
   P.N = c->N;
   for (int k = 0; k < 2; ++k) {
@@ -1049,7 +1073,8 @@ static mc_status complete_step(mc_ctx* c, int scheme, mc_step_report* out) {
                        : rep.status == MC_ERR_BREAKDOWN ? "CG breakdown (p.q <= 0)"
                                                         : "step skipped after an earlier failure";
     return fail(c, (mc_status)rep.status, "step %d (%s), solve %d: %s after %lld iterations; state not advanced",
-                c->step_no + 1, scheme == MC_COUPLED ? "coupled" : "D-scheme", rep.failed_solve, what,
+                c->step_no + 1, scheme == MC_COUPLED ? "coupled" : scheme == MC_DECOUPLED_D ? "D-scheme"
+                : scheme == MC_DECOUPLED_L ? "L-scheme" : "U-scheme", rep.failed_solve, what,
                 rep.failed_solve >= 0 ? (long long)rep.iters[rep.failed_solve] : 0LL);
   }
   return MC_OK;
@@ -1057,6 +1082,9 @@ static mc_status complete_step(mc_ctx* c, int scheme, mc_step_report* out) {
 
 static mc_status do_step(mc_ctx* c, int scheme, mc_step_report* rep) {
   if (!c) return fail(c, MC_ERR_ARG, "NULL context");
+  if (scheme < MC_COUPLED || scheme > MC_DECOUPLED_U) return fail(c, MC_ERR_ARG, "unknown scheme %d", scheme);
+  if ((scheme == MC_DECOUPLED_L || scheme == MC_DECOUPLED_U) && !c->has_korder)
+    return fail(c, MC_ERR_STATE, "L/U scheme before mc_set_permeability_order");
   mc_status st = finalize(c);
   if (st != MC_OK) return st;
   CUDA_TRY(c, cudaMemsetAsync(c->fail, 0, 4, c->stream));
@@ -1072,12 +1100,30 @@ extern "C" mc_status mc_step_coupled(mc_ctx* c, mc_step_report* rep) {
   return do_step(c, MC_COUPLED, rep);
 }
 
+extern "C" mc_status mc_step(mc_ctx* c, int32_t scheme, mc_step_report* rep) { return do_step(c, scheme, rep); }
+
+extern "C" mc_status mc_set_permeability_order(mc_ctx* c, const int32_t* order) {
+  if (!c || !order) return fail(c, MC_ERR_ARG, "NULL argument");
+  std::vector<int32_t> o;
+  mc_status st = fetch(c, o, order, c->L);
+  if (st != MC_OK) return st;
+  std::vector<int32_t> srt(o);
+  std::sort(srt.begin(), srt.end());
+  for (int a = 0; a < c->L; ++a)
+    if (srt[(size_t)a] != a) return fail(c, MC_ERR_ARG, "permeability order is not a permutation of 0..%d", c->L - 1);
+  for (int a = 0; a < c->L; ++a) c->korder[a] = o[(size_t)a];
+  c->has_korder = true;
+  for (auto& pl : c->plan) pl.valid = false;
+  c->uploaded_plan = -1;
+  return MC_OK;
+}
+
 static mc_status copy_out(mc_ctx* c, int a, double* dst);
 
 extern "C" mc_status mc_run(mc_ctx* c, int32_t scheme, int32_t n_steps, mc_step_report* reps,
                             double* const* snapshots) {
   if (!c) return fail(c, MC_ERR_ARG, "NULL context");
-  if (scheme != MC_COUPLED && scheme != MC_DECOUPLED_D) return fail(c, MC_ERR_ARG, "unknown scheme %d", scheme);
+  if (scheme < MC_COUPLED || scheme > MC_DECOUPLED_U) return fail(c, MC_ERR_ARG, "unknown scheme %d", scheme);
   if (n_steps < 0) return fail(c, MC_ERR_ARG, "n_steps < 0");
   mc_status st = finalize(c);
   if (st != MC_OK) return st;

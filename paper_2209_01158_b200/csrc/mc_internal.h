@@ -95,6 +95,7 @@ struct StepParams {
   ContDev cont[MC_MAX_CONTINUA];
   Group grp[MC_MAX_CONTINUA];
   int32_t L, ngroups, nphases, coupled, total_ctas;
+  int32_t gs;              // L/U schemes: transfer from continua of earlier phases at layer n
   int64_t N;               // padded global size
   // state and CG work vectors (global DOF space, padded)
   double* u[2];            // ping-pong state: u[cur] = p^{n-1}, u[cur^1] = iterate x

@@ -911,7 +911,7 @@ __device__ void iter_graph8(const Ctx& c, const ContDev& C, int r0, int r1,
 // b = (m/tau) u + F + [D: sum sigma u_other];  r0 = b - K u;  x = u;  p0 = q0 = 0
 template <bool CPL>
 __device__ __forceinline__ void init_row(const StepParams& P, int64_t gi, double Ku_nb,
-                                         const double* uo, double* x, double (&acc)[3]) {
+                                         const double* uo, double* x, int myphase, double (&acc)[3]) {
   const double u = uo[gi];
   double b = ldro(P.mtau + gi) * u + ldro(P.F + gi);
   double Ku = ldro((CPL ? P.dsC : P.dsD) + gi) * u + Ku_nb;
@@ -919,8 +919,19 @@ __device__ __forceinline__ void init_row(const StepParams& P, int64_t gi, double
   for (int32_t e = e0; e < e1; ++e) {
     const int32_t j = ldro(P.cidx + e);
     const double s = ldro(P.cval + e);
-    if (CPL) Ku += s * (u - uo[j]);
-    else b += s * uo[j];     // lagged transfer Q_ab u_b^{n-1}
+    if (CPL) {
+      Ku += s * (u - uo[j]);
+    } else {
+      // D-scheme: Q_ab u_b^{n-1}.  L/U schemes: continua solved
+      // earlier in this step contribute their layer-n value.
+      const double* src = uo;
+      if (P.gs) {
+        int bc = 0;
+        while (bc + 1 < P.L && j >= P.cont[bc + 1].off) ++bc;
+        if (P.grp[bc].phase < myphase) src = x;
+      }
+      b += s * src[j];
+    }
   }
   const double r = b - Ku;
   x[gi] = u;
@@ -933,7 +944,7 @@ __device__ __forceinline__ void init_row(const StepParams& P, int64_t gi, double
 }
 
 template <bool CPL>
-__device__ void init_item(const StepParams& P, const Item& it, const double* uo, double* x,
+__device__ void init_item(const StepParams& P, const Item& it, const double* uo, double* x, int myphase,
                           double (&acc)[3]) {
   const ContDev& C = P.cont[it.cont];
   const int lane = threadIdx.x & 31;
@@ -948,7 +959,7 @@ __device__ void init_item(const StepParams& P, const Item& it, const double* uo,
       if (col + 1 < nx) s += ldro(C.Tx + i) * (u - uo[gi + 1]);
       if (y > 0) s += ldro(C.Ty + i - nx) * (u - uo[gi - nx]);
       if (y + 1 < ny) s += ldro(C.Ty + i) * (u - uo[gi + nx]);
-      init_row<CPL>(P, gi, s, uo, x, acc);
+      init_row<CPL>(P, gi, s, uo, x, myphase, acc);
     }
   } else {
     for (int i = it.a + lane; i < it.b; i += 32) {
@@ -960,7 +971,7 @@ __device__ void init_item(const StepParams& P, const Item& it, const double* uo,
         const double t = C.val ? ldro(C.val + e) : C.Tconst;
         s += t * (u - uo[ldro(C.col + e)]);
       }
-      init_row<CPL>(P, gi, s, uo, x, acc);
+      init_row<CPL>(P, gi, s, uo, x, myphase, acc);
     }
   }
 }
@@ -1053,9 +1064,9 @@ __device__ void run_group(const StepParams& P, int g, int cl, double* x, const d
         rit.kind = ITEM_GRAPH;
         rit.a = 32 * m;
         rit.b = (int32_t)min((int64_t)(32 * m + 32), P.cont[k].n);
-        init_item<CPL>(P, rit, uo, x, a3);
+        init_item<CPL>(P, rit, uo, x, G.phase, a3);
       }
-  for (int it = ib + wg; it < ie; it += W) init_item<CPL>(P, P.items[it], uo, x, a3);
+  for (int it = ib + wg; it < ie; it += W) init_item<CPL>(P, P.items[it], uo, x, G.phase, a3);
   unsigned long long epoch = 0;
   double t3[3];
   group_allreduce<3>(P, g, cl, epoch, a3, t3);

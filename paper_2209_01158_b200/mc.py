@@ -18,7 +18,8 @@ LIB_PATH = os.path.join(_HERE, "libmc.so")
 
 MC_OK, MC_ERR_ARG, MC_ERR_STATE, MC_ERR_NOMEM, MC_ERR_CUDA, MC_ERR_NOCONV, MC_ERR_BREAKDOWN = range(7)
 MC_GRID2D, MC_GRAPH = 0, 1
-MC_COUPLED, MC_DECOUPLED_D = 0, 1
+MC_COUPLED, MC_DECOUPLED_D, MC_DECOUPLED_L, MC_DECOUPLED_U = 0, 1, 2, 3
+SCHEMES = {"coupled": MC_COUPLED, "D": MC_DECOUPLED_D, "L": MC_DECOUPLED_L, "U": MC_DECOUPLED_U}
 MC_MAX_CONTINUA = 4
 STATUS_NAMES = {0: "MC_OK", 1: "MC_ERR_ARG", 2: "MC_ERR_STATE", 3: "MC_ERR_NOMEM", 4: "MC_ERR_CUDA",
                 5: "MC_ERR_NOCONV", 6: "MC_ERR_BREAKDOWN"}
@@ -63,6 +64,7 @@ class mc_step_report(C.Structure):
 
 
 EXPORTS = ["mc_create", "mc_set_continuum", "mc_set_coupling", "mc_step_decoupled", "mc_step_coupled",
+           "mc_step", "mc_set_permeability_order",
            "mc_run", "mc_get_state", "mc_set_state", "mc_size", "mc_last_kernel_ms", "mc_destroy",
            "mc_error_string", "mc_abi_version"]
 
@@ -85,6 +87,8 @@ def load(path: str | None = None):
     lib.mc_set_coupling.argtypes = [P, C.POINTER(mc_coupling_desc)]
     lib.mc_step_decoupled.argtypes = [P, C.POINTER(mc_step_report)]
     lib.mc_step_coupled.argtypes = [P, C.POINTER(mc_step_report)]
+    lib.mc_step.argtypes = [P, _i32, C.POINTER(mc_step_report)]
+    lib.mc_set_permeability_order.argtypes = [P, C.c_void_p]
     lib.mc_run.argtypes = [P, _i32, _i32, C.POINTER(mc_step_report), C.POINTER(C.c_void_p)]
     lib.mc_get_state.argtypes = [P, _i32, C.c_void_p]
     lib.mc_set_state.argtypes = [P, _i32, C.c_void_p]
@@ -107,6 +111,22 @@ class MCError(RuntimeError):
         super().__init__(f"{STATUS_NAMES.get(status, status)}: {msg}")
         self.status = status
         self.report = report
+
+
+def permeability_order(scn):
+    """Continuum ids by ascending permeability: the scenario's k
+    (geometric mean of a k field), the fracture's k_f, NLMC k_scale (marshalling of a
+    physical description, the order itself is a caller input of the ABI)."""
+    if scn["kind"] == "fine":
+        ks = []
+        for c in scn["continua"]:
+            k = c["k"]
+            ks.append(float(np.exp(np.mean(np.log(k)))) if np.ndim(k) else float(k))
+    elif scn["kind"] == "nlmc":
+        ks = [float(np.mean(scn["within"][a][2])) for a in range(2)]
+    else:
+        return None
+    return [int(a) for a in np.argsort(ks, kind="stable")]
 
 
 def _ptr(a, ctype=_pd):
@@ -155,6 +175,10 @@ class Problem:
             self._check(self.lib.mc_set_coupling(self.ctx, C.byref(d)))
         self._keep = []
         self.sizes = [int(self.lib.mc_size(self.ctx, a)) for a in range(self.L)]
+        self.korder = permeability_order(scn)
+        if self.korder is not None:
+            arr = np.asarray(self.korder, dtype=np.int32)
+            self._check(self.lib.mc_set_permeability_order(self.ctx, arr.ctypes.data_as(C.c_void_p)))
 
     # ------------------------------------------------------------------ marshalling
     def _arr(self, x, dtype):
@@ -239,8 +263,7 @@ class Problem:
 
     def step(self, scheme="D"):
         rep = mc_step_report()
-        fn = self.lib.mc_step_coupled if scheme == "coupled" else self.lib.mc_step_decoupled
-        st = fn(self.ctx, C.byref(rep))
+        st = self.lib.mc_step(self.ctx, SCHEMES[scheme], C.byref(rep))
         self._check(st, report=rep.as_dict())
         return rep.as_dict()
 
@@ -251,8 +274,7 @@ class Problem:
         if snapshots is not None:
             flat = [snapshots[s][a] for s in range(n_steps) for a in range(self.L)]
             snaps = (C.c_void_p * len(flat))(*[C.c_void_p(t.data_ptr()) for t in flat])
-        sch = MC_COUPLED if scheme == "coupled" else MC_DECOUPLED_D
-        st = self.lib.mc_run(self.ctx, sch, n_steps, reps, snaps)
+        st = self.lib.mc_run(self.ctx, SCHEMES[scheme], n_steps, reps, snaps)
         out = [reps[s].as_dict() for s in range(n_steps)]
         self._check(st, report=out)
         return out

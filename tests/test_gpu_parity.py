@@ -40,10 +40,16 @@ def gpu_traj(scn, scheme, steps, **kw):
     return out, reps
 
 
+def k_order(scn):
+    """Continua by ascending permeability for the L/U schemes: in every
+    workload here the continuum index already ascends with k (matrix < natural < fracture)."""
+    return list(range(len(scn["continua"]) if scn["kind"] == "fine" else 2))
+
+
 def oracle_traj(scn, scheme, steps, tau=None):
     sys_ = asm.assemble(scn)
     tau = scn["T"] / scn["NT"] if tau is None else tau
-    return [sys_.split(u) for u in schemes.run(sys_, scheme, tau, steps)]
+    return [sys_.split(u) for u in schemes.run(sys_, scheme, tau, steps, order_by_k=k_order(scn))]
 
 
 def assert_parity(got, ref, tol=TOL):
@@ -132,9 +138,47 @@ def test_config2_standin_three_continua(torch_cuda, scheme):
     assert_parity(got, ref)
 
 
+# ---------------------------------------------------------------- L- and U-schemes
+@pytest.mark.parametrize("scheme", ["L", "U"])
+def test_LU_config0_config3(torch_cuda, scheme):
+    for cid in (0, 3):
+        scn = make(cid)
+        got, _ = gpu_traj(scn, scheme, 25)
+        assert_parity(got, oracle_traj(scn, scheme, 25))
+
+
+@pytest.mark.parametrize("scheme", ["L", "U"])
+def test_LU_config1_and_three_continua(torch_cuda, scheme):
+    scn = make(1)
+    got, _ = gpu_traj(scn, scheme, 10)
+    assert_parity(got, oracle_traj(scn, scheme, 10))
+    p = dict(CONFIGS[2])
+    p.pop("kind")
+    p.update(n=256, segments=1500 * 256 // 2048, lengths=(100 * 256 // 2048, 800 * 256 // 2048))
+    scn = make_fine(**p)
+    got, _ = gpu_traj(scn, scheme, 15)
+    assert_parity(got, oracle_traj(scn, scheme, 15))
+
+
+def test_LU_needs_order(torch_cuda):
+    from paper_2209_01158_b200 import mc
+    lib = mc.load()
+    ctx = C.c_void_p()
+    assert lib.mc_create(C.byref(ctx), 1, C.byref(mc.mc_options(tau=0.1))) == 0
+    d = mc.mc_continuum_desc(kind=mc.MC_GRID2D, n=4, nx=2, ny=2, h=0.5, k_const=1.0, c_const=1.0)
+    assert lib.mc_set_continuum(ctx, 0, C.byref(d)) == 0
+    assert lib.mc_step(ctx, mc.MC_DECOUPLED_U, None) == mc.MC_ERR_STATE
+    bad = np.array([1], dtype=np.int32)
+    assert lib.mc_set_permeability_order(ctx, bad.ctypes.data_as(C.c_void_p)) == mc.MC_ERR_ARG
+    ok = np.array([0], dtype=np.int32)
+    assert lib.mc_set_permeability_order(ctx, ok.ctypes.data_as(C.c_void_p)) == 0
+    assert lib.mc_step(ctx, mc.MC_DECOUPLED_U, None) == 0
+    lib.mc_destroy(ctx)
+
+
 # ---------------------------------------------------------------- ragged / edge cases
 @pytest.mark.parametrize("n,segs", [(1, 0), (3, 1), (37, 4), (45, 7)])
-@pytest.mark.parametrize("scheme", ["D", "coupled"])
+@pytest.mark.parametrize("scheme", ["D", "coupled", "U"])
 def test_ragged_small(torch_cuda, n, segs, scheme):
     scn = make_fine(n, seed=n, T=1, NT=8, segments=segs, lengths=(1, max(1, n // 2)), k_sigma=1.0,
                     k_f=1e4, c_f=0.01, sigma_f=("k_m", 100.0))

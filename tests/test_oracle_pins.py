@@ -492,3 +492,134 @@ def test_refinement_reaches_exact_fracture_plateau():
     uf = schemes.run(sys_, "D", tau, 1, u0=u)[0][n * n:]
     mt = 0.01 * (1.0 / n) / tau
     assert np.max(np.abs(uf - 1.0 / (1.0 + mt))) <= 1e-15
+
+
+# ---------------------------------------------------------------- L- and U-schemes
+def test_LU_one_cell_worked_example():
+    g = GOLD["one_cell_two_continua_LU"]
+    base = GOLD["one_cell_two_continua"]
+    sys_ = _one_cell_system(base["c"], base["sigma"])
+    for k in ("L", "U"):
+        u = schemes.run(sys_, k, base["tau"], 1, u0=np.array(base["u0"]), order_by_k=g["order_by_k"])[0]
+        assert np.allclose(u, g[k], rtol=1e-15, atol=1e-16)
+
+
+@pytest.mark.parametrize("kind", ["L", "U"])
+def test_LU_0d_closed_form(kind):
+    n, c1, c2, sig, tau = 4, 1.0, 0.1, 5.0, 0.05
+    scn = make_fine(n, seed=0, T=1, NT=1, segments=0, lengths=(1, 1), c_m=c1,
+                    natural=dict(k=1e2, c=c2, sigma_12=sig, sigma_2f=0.0), dirichlet=None)
+    sys_ = asm.assemble(scn)
+    a, b = 0.7, -0.3
+    u = np.concatenate([np.full(n * n, a), np.full(n * n, b)])
+    traj = schemes.run(sys_, kind, tau, 10, u0=u, order_by_k=[0, 1])
+    h2 = (1.0 / n) ** 2
+    m1, m2, s = c1 * h2, c2 * h2, sig * h2
+    v1, v2 = a, b
+    for uk in traj:
+        if kind == "L":                 # continuum 0 first (old v2), then 1 with the new v1
+            v1 = (m1 * v1 + tau * s * v2) / (m1 + tau * s)
+            v2 = (m2 * v2 + tau * s * v1) / (m2 + tau * s)
+        else:                           # continuum 1 first, then 0 with the new v2
+            v2 = (m2 * v2 + tau * s * v1) / (m2 + tau * s)
+            v1 = (m1 * v1 + tau * s * v2) / (m1 + tau * s)
+        assert np.max(np.abs(uk[: n * n] - v1)) <= 1e-12 and np.max(np.abs(uk[n * n:] - v2)) <= 1e-12
+
+
+def dense_seq_steps(off, A, M, F, tau, u, steps, order):
+    """Literal block Gauss-Seidel in `order` on a dense system (brute force for L/U)."""
+    out = []
+    L = len(off) - 1
+    for _ in range(steps):
+        new = u.copy()
+        for a in order:
+            s = slice(off[a], off[a + 1])
+            b = M[s] / tau * u[s] + F[s]
+            for c in range(L):
+                if c != a:
+                    b -= A[s, off[c]:off[c + 1]] @ new[off[c]:off[c + 1]]
+            new[s] = np.linalg.solve(np.diag(M[s] / tau) + A[s, s], b)
+        u = new
+        out.append(u.copy())
+    return out
+
+
+@pytest.mark.parametrize("kind", ["L", "U"])
+def test_LU_bruteforce_three_continua(kind):
+    scn = make_fine(4, seed=21, T=1, NT=6, segments=2, lengths=(2, 3), k_sigma=1.0, k_f=1e4, c_f=0.01,
+                    sigma_f=("k_m", 100.0), natural=dict(k=1e2, c=0.1, sigma_12=5.0, sigma_2f=50.0))
+    off, A, M, F = dense_fine_bruteforce(scn)
+    order = [0, 1, 2]                                   # k: matrix 1 < natural 1e2 < fracture 1e4
+    ref = dense_seq_steps(off, A, M, F, 1.0 / 6, np.zeros(off[-1]), 6, order if kind == "L" else order[::-1])
+    got = schemes.run(asm.assemble(scn), kind, 1.0 / 6, 6, order_by_k=order)
+    for r, g in zip(ref, got):
+        assert rel(g, r) <= 1e-13
+
+
+def test_LU_sigma_zero_equal_coupled():
+    p = dict(n=64, seed=0, T=1.0, NT=10, segments=6, lengths=(10, 40), k_f=1e4, c_f=0.01,
+             sigma_f=("const", 0.0))
+    sys_ = asm.assemble(make_fine(**p))
+    tc = schemes.run(sys_, "coupled", 0.1, 5)
+    for k in ("L", "U"):
+        for a, b in zip(tc, schemes.run(sys_, k, 0.1, 5, order_by_k=[0, 1])):
+            assert rel(b, a) <= 1e-12
+
+
+@pytest.mark.parametrize("kind", ["L", "U"])
+def test_LU_A_norm_monotone(kind):                       # Theorem 3 holds for L/U (PAPER.md:582)
+    scn = make_fine(32, seed=9, T=1, NT=30, segments=5, lengths=(4, 12), k_sigma=1.0,
+                    dirichlet=(0.0, 0.0), sigma_f=("k_m", 100.0), k_f=1e4)
+    sys_ = asm.assemble(scn)
+    u0 = np.random.default_rng(2).standard_normal(sum(sys_.sizes))
+    prev = float(u0 @ (sys_.A @ u0))
+    for u in schemes.run(sys_, kind, 1.0 / 30, 30, u0=u0, order_by_k=[0, 1]):
+        cur = float(u @ (sys_.A @ u))
+        assert cur <= prev * (1 + 1e-8)
+        prev = cur
+
+
+@pytest.mark.parametrize("kind", ["L", "U"])
+def test_LU_mass_balance(kind):
+    """Summing the rows: sum m du = tau [boundary inflow - sum over LAGGED transfer entries of
+    sigma * du(of the continuum solved later)] — only the lagged half of Q leaves a defect."""
+    scn = make(0)
+    sys_ = asm.assemble(scn)
+    tau = scn["T"] / scn["NT"]
+    n, h = scn["n"], scn["h"]
+    m = np.concatenate([np.full(n * n, scn["continua"][0]["c"] * h * h),
+                        np.full(len(scn["fracture"]["cells"]), scn["continua"][1]["c"] * h)])
+    host = scn["fracture"]["cells"]
+    sig = scn["couplings"][0]["sigma"]
+    traj = [sys_.u0] + schemes.run(sys_, kind, tau, 20, order_by_k=[0, 1])
+    for k in range(1, len(traj)):
+        du = traj[k] - traj[k - 1]
+        flux, gross = _boundary_flux(scn, traj[k][: n * n])
+        # L: matrix (0) first -> its rows lag the fracture: defect sigma * du_fracture
+        # U: fracture first -> its rows lag the matrix: defect sigma * du_matrix(host)
+        lag = du[n * n:] if kind == "L" else du[host]
+        rhs = tau * flux - tau * np.sum(sig * lag)
+        assert abs(np.sum(m * du) - rhs) <= 1e-8 * tau * gross
+
+
+@pytest.mark.parametrize("kind", ["L", "U"])
+def test_LU_first_order_in_tau(kind):
+    errs = []
+    for NT in (100, 200, 400, 800):
+        sys_ = asm.assemble(make(0))
+        T = 0.002
+        uc = schemes.run(sys_, "coupled", T / NT, NT)[-1]
+        ud = schemes.run(sys_, kind, T / NT, NT, order_by_k=[0, 1])[-1]
+        errs.append(rel(ud, uc))
+    ratios = [errs[i] / errs[i + 1] for i in range(3)]
+    assert all(1.7 <= r <= 2.3 for r in ratios), ratios
+
+
+def test_U_more_accurate_than_D_paper_pattern():
+    """PAPER.md:956 (and Tables 1-4): the U-scheme is the most accurate decoupled scheme.
+    Checked on config-0 inputs at the paper's T = 0.002."""
+    sys_ = asm.assemble(make(0))
+    T, NT = 0.002, 50
+    uc = schemes.run(sys_, "coupled", T / NT, NT)[-1]
+    e = {k: rel(schemes.run(sys_, k, T / NT, NT, order_by_k=[0, 1])[-1], uc) for k in ("D", "L", "U")}
+    assert e["U"] < e["D"], e
