@@ -865,14 +865,15 @@ static Plan make_plan(const mc_ctx* c, int scheme) {
       Group& g = P.grp[a];
       g.phase = pos;
       g.cta_begin = 0;
-      g.cta_count = T;
+      // a latency-bound solve pays for every CTA in its barrier: use what it can use
+      g.cta_count = c->hc[a].n >= kLargeRows ? T : std::min(T, useful_ctas(c->hc[a]));
       g.tol2 = c->hc[a].rtol * c->hc[a].rtol;
       g.maxit = default_maxit(c, c->hc[a].n);
       g.cont_mask = 1 << a;
     }
     for (int a = 0; a < L; ++a) {
       P.grp[a].item_begin = (int32_t)P.items.size();
-      add_items(c, a, T * kWarps, P.items);
+      add_items(c, a, P.grp[a].cta_count * kWarps, P.items);
       P.grp[a].item_count = (int32_t)P.items.size() - P.grp[a].item_begin;
     }
     P.valid = true;
@@ -890,7 +891,7 @@ static Plan make_plan(const mc_ctx* c, int scheme) {
     for (int a = 0; a < L; ++a) {
       P.grp[a].phase = a;
       P.grp[a].cta_begin = 0;
-      ctas[a] = T;
+      ctas[a] = c->hc[a].n >= kLargeRows ? T : std::min(T, useful_ctas(c->hc[a]));
     }
   } else {
     // one phase: CTAs split by work (rows x last iterations), each solve guaranteed the

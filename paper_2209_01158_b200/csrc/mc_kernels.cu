@@ -879,28 +879,64 @@ __device__ void iter_graph(const Ctx& c, const ContDev& C, int r0, int r1,
 template <bool CPL>
 __device__ void iter_graph8(const Ctx& c, const ContDev& C, int r0, int r1,
                             double (&acc)[kNPart]) {
+  // lane `sub` of a row's 8 lanes takes edges (and, coupled, transfer entries) sub,
+  // sub+8, sub+16, sub+24: all their column / value loads issue together, then all
+  // neighbour gathers, so a row costs ~3 memory trips however long it is (<= 32 entries
+  // per list in one batch; longer lists loop)
   const int lane = threadIdx.x & 31, sub = lane & 7, grp = lane >> 3;
   for (int base = r0; base < r1; base += 4) {
     const int i = base + grp;
     const bool ok = i < r1;
     const int64_t gi = C.off + (ok ? i : r0);
+    const int32_t e0 = ok ? ldro(C.rowptr + i) : 0, e1 = ok ? ldro(C.rowptr + i + 1) : 0;
+    int32_t f0 = 0, f1 = 0;
+    if (CPL && ok) {
+      f0 = ldro(c.P->cptr + gi);
+      f1 = ldro(c.P->cptr + gi + 1);
+    }
     double pc = 0.0, rc = 0.0, dc = 0.0;
     if (ok && sub == 0) c.own(gi, pc, rc, dc);
-    pc = __shfl_sync(0xffffffffu, pc, lane & ~7);
-    double s = 0.0;
-    if (ok) {
-      const int32_t e0 = ldro(C.rowptr + i), e1 = ldro(C.rowptr + i + 1);
-      for (int32_t e = e0 + sub; e < e1; e += 8) {
-        const double t = C.val ? ldro(C.val + e) : C.Tconst;
-        s += t * (pc - c.pn_at(ldro(C.col + e)));
+    // first batch (<= 32 entries per list): every load issues before pc is needed
+    double pj[4], tj[4], pf[4], tf[4];
+    // unconditional loads (an unused slot reads entry 0 / this row and is discarded):
+    // no branch separates the loads, so they all issue in one batch
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int32_t e = e0 + sub + 8 * k;
+      const bool use = e < e1;
+      const int32_t ee = use ? e : 0;
+      const int32_t jr = ldro(C.col + ee);
+      const double tv = C.val ? ldro(C.val + ee) : C.Tconst;
+      tj[k] = use ? tv : 0.0;
+      pj[k] = c.pn_at(use ? (int64_t)jr : gi);
+      if (CPL) {
+        const int32_t f = f0 + sub + 8 * k;
+        const bool usef = f < f1;
+        const int32_t ff = usef ? f : 0;
+        const int32_t jf = ldro(c.P->cidx + ff);
+        const double tv2 = ldro(c.P->cval + ff);
+        tf[k] = usef ? tv2 : 0.0;
+        pf[k] = c.pn_at(usef ? (int64_t)jf : gi);
       }
     }
+    pc = __shfl_sync(0xffffffffu, pc, lane & ~7);                 // all lanes, uniform
+    double s = 0.0;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) s += tj[k] * (pc - pj[k]);
+    if (CPL) {
+#pragma unroll
+      for (int k = 0; k < 4; ++k) s += tf[k] * (pc - pf[k]);
+    }
+    // rare: longer lists
+    for (int32_t e = e0 + 32 + sub; e < e1; e += 8)
+      s += (C.val ? ldro(C.val + e) : C.Tconst) * (pc - c.pn_at(ldro(C.col + e)));
+    if (CPL)
+      for (int32_t f = f0 + 32 + sub; f < f1; f += 8) s += ldro(c.P->cval + f) * (pc - c.pn_at(ldro(c.P->cidx + f)));
     s += __shfl_xor_sync(0xffffffffu, s, 4);
     s += __shfl_xor_sync(0xffffffffu, s, 2);
     s += __shfl_xor_sync(0xffffffffu, s, 1);
     if (ok && sub == 0) {
-      double qv = ldro(c.ds + gi) * pc + s;
-      if (CPL) qv += c.couple_q(gi, pc);
+      const double qv = ldro(c.ds + gi) * pc + s;
       stmut(c.qd + gi, qv);
       c.accum(acc, pc, rc, dc, qv);
     }
