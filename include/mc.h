@@ -124,6 +124,12 @@ typedef struct {
   double rtol;                                   /* this continuum's D-scheme CG tolerance;
                                                     <= 0: mc_options.rtol.  The coupled solve
                                                     uses the smallest over all continua.    */
+  const double* well_q;                          /* NULL, or per cell well index q_w >= 0:
+                                                    source f = q_w (p_w - p) (PAPER.md:834,
+                                                    injection sign of SPEC.md:154), i.e.
+                                                    q_w|cell| on the diagonal and
+                                                    q_w p_w |cell| in F                     */
+  double well_p;                                 /* p_w                                    */
 } mc_continuum_desc;
 
 /*

@@ -15,6 +15,7 @@ from .generator import (  # noqa: F401
     make,
     make_fine,
     crop_fine,
+    make_paper_analogue,
     make_nlmc,
     fracture_network,
 )

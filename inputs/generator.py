@@ -212,6 +212,47 @@ def make_nlmc(nc: int = 256, *, seed: int = 3, T: float = 1.0, NT: int = 100, c=
                 between=between, dirichlet=dirichlet)
 
 
+def make_paper_analogue(kind: str = "2C", n: int = 200, seed: int = 32, segments: int = 25,
+                        lengths=(120, 240), T: float = 0.002, NT: int = 50) -> dict:
+    """The paper's own test setting with a synthetic network in place
+    of the unpublished 25-fracture geometry: unit square, n x n grid,
+    25 axis-aligned segments (C4 rules; seed and lengths chosen so the network has 2 667
+    cells, the paper's 2 684), homogeneous Neumann boundaries, p_alpha^0 = 1,
+    T = 0.002, N_T = 50, wells in the fracture cells whose host cell centre lies in
+    [0.1,0.15]^2 or [0.6,0.65]x[0.85,0.9] with q_w = 1e5, p_w = 1.2 (PAPER.md:834).
+    2C: matrix c=0.1, k=1; fracture c=1, k=1e6.  3C: matrix c=0.05,
+    k=1e-3; natural fractures c=0.1, k=1; hydraulic fractures c=1, k=1e6.
+    Readings (C26-C28): matrix-fracture transfer sigma = 4 k of the Omega
+    continuum (EFM |E|/d with the SPEC.md:68 mean distance h/4); co-located
+    sigma_12 = k_1; wells as injection q_w (p_w - p) on the fracture."""
+    rng = np.random.default_rng(seed)
+    cells, edges = fracture_network(n, rng, segments, lengths)
+    h = 1.0 / n
+    cy, cx = np.divmod(cells, n)
+    xc, yc = (cx + 0.5) * h, (cy + 0.5) * h
+    box = ((xc >= 0.1) & (xc <= 0.15) & (yc >= 0.1) & (yc <= 0.15)) | \
+          ((xc >= 0.6) & (xc <= 0.65) & (yc >= 0.85) & (yc <= 0.9))
+    well_q = np.where(box, 1e5, 0.0)
+    if kind == "2C":
+        omega = [dict(name="matrix", kind="grid", k=1.0, c=0.1, dirichlet=None, u0=1.0)]
+        frac = dict(name="fracture", kind="fracture", k=1e6, c=1.0, dirichlet=None, u0=1.0,
+                    well_q=well_q, well_p=1.2)
+        couplings = [dict(a=0, b=1, type="embedded", sigma=np.full(len(cells), 4.0 * 1.0))]
+    elif kind == "3C":
+        omega = [dict(name="matrix", kind="grid", k=1e-3, c=0.05, dirichlet=None, u0=1.0),
+                 dict(name="natural", kind="grid", k=1.0, c=0.1, dirichlet=None, u0=1.0)]
+        frac = dict(name="fracture", kind="fracture", k=1e6, c=1.0, dirichlet=None, u0=1.0,
+                    well_q=well_q, well_p=1.2)
+        couplings = [dict(a=0, b=1, type="colocated", sigma=1e-3),
+                     dict(a=0, b=2, type="embedded", sigma=np.full(len(cells), 4.0 * 1e-3)),
+                     dict(a=1, b=2, type="embedded", sigma=np.full(len(cells), 4.0 * 1.0))]
+    else:
+        raise ValueError(kind)
+    return dict(kind="fine", config_id=None, conv_version=CONV_VERSION, seed=seed, n=int(n), h=h,
+                T=float(T), NT=int(NT), continua=omega + [frac],
+                fracture=dict(cells=cells, edges=edges), couplings=couplings, paper_analogue=kind)
+
+
 def crop_fine(scn: dict, m: int) -> dict:
     """The sub-square [0, m)^2 of a fine scenario: same cells (h unchanged), the k field,
     fracture cells hosted inside, fracture edges with both ends inside, their transfer

@@ -184,7 +184,15 @@ def assemble_fine(scn) -> System:
             Q[(a, b)] = sp.diags(np.full(sizes[a], float(cp["sigma"]) * h * h))   # C9
         else:
             raise ValueError(cp["type"])
-    u0 = [np.zeros(s) for s in sizes]                        # u0 = 0 (C17)
+    u0 = [np.full(s, float(c.get("u0", 0.0))) for s, c in zip(sizes, scn["continua"])]   # C17
+    # wells f = q_w (p_w - p) on a continuum (paper analogue; sign per
+    # SPEC.md:154): q_w |cell| on the diagonal, q_w p_w |cell| in F
+    for a, c in enumerate(scn["continua"]):
+        if "well_q" in c:
+            meas = h * h if c["kind"] == "grid" else h
+            wq = np.asarray(c["well_q"], dtype=np.float64) * meas
+            Ds[a] = sp.csr_matrix(Ds[a] + sp.diags(wq))
+            Fs[a] = Fs[a] + wq * float(c["well_p"])
     return block_system(sizes, Ds, Ms, Fs, Q, u0, names)
 
 
@@ -322,6 +330,8 @@ def flux_form(scn, sys_: System) -> FluxForm:
                 EJ.append(off[a] + fj)
                 ET.append(face_transmissibility(cont["k"], fi, fj))
                 BT.append(np.zeros(len(fi), dtype=bool))
+                if "well_q" in cont:                                            # wells
+                    diag[off[a]:off[a + 1]] += np.asarray(cont["well_q"], dtype=np.float64) * h * h
                 if cont["dirichlet"] is not None:
                     kk = np.full(n * n, float(cont["k"])) if np.ndim(cont["k"]) == 0 else cont["k"]
                     ix = np.arange(n * n) % n
@@ -331,6 +341,8 @@ def flux_form(scn, sys_: System) -> FluxForm:
                             diag[off[a] + cells] += kk[cells] * h / (h / 2.0)     # C3
             else:
                 e = np.asarray(scn["fracture"]["edges"], dtype=np.int64).reshape(-1, 2)
+                if "well_q" in cont:                                            # wells
+                    diag[off[a]:off[a + 1]] += np.asarray(cont["well_q"], dtype=np.float64) * h
                 EI.append(off[a] + e[:, 0])
                 EJ.append(off[a] + e[:, 1])
                 ET.append(np.full(len(e), float(cont["k"]) / h))                 # C7

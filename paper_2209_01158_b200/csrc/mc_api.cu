@@ -249,6 +249,23 @@ extern "C" int64_t mc_size(const mc_ctx* c, int32_t alpha) {
 }
 
 // ====================================================================== continua
+// wells f = q_w (p_w - p): q_w |cell| on the diagonal (both schemes), q_w p_w |cell| in F
+static mc_status add_wells(mc_ctx* c, HostCont& H, const mc_continuum_desc* d, double meas_const) {
+  if (!d->well_q) return MC_OK;
+  if (!std::isfinite(d->well_p)) return fail(c, MC_ERR_ARG, "well_p not finite");
+  std::vector<double> q;
+  mc_status st = field(c, q, d->well_q, 0.0, H.n, "well_q", false);
+  if (st != MC_OK) return st;
+  for (int64_t i = 0; i < H.n; ++i) {
+    const size_t s = (size_t)i;
+    if (!H.fixed.empty() && H.fixed[s]) continue;
+    const double w = q[s] * (meas_const > 0.0 ? meas_const : H.measure[s]);
+    H.dbase[s] += w;
+    H.F[s] += w * d->well_p;
+  }
+  return MC_OK;
+}
+
 static mc_status set_grid(mc_ctx* c, HostCont& H, const mc_continuum_desc* d) {
   const int64_t n = d->n;
   if (d->nx < 1 || d->ny < 1 || (int64_t)d->nx * d->ny != n)
@@ -313,7 +330,7 @@ static mc_status set_grid(mc_ctx* c, HostCont& H, const mc_continuum_desc* d) {
       H.dbase[i] = H.mtau[i] + db;
       H.F[i] = Fi;
     }
-  return MC_OK;
+  return add_wells(c, H, d, area);
 }
 
 static mc_status set_graph(mc_ctx* c, HostCont& H, const mc_continuum_desc* d) {
@@ -446,7 +463,7 @@ static mc_status set_graph(mc_ctx* c, HostCont& H, const mc_continuum_desc* d) {
     H.val = std::move(vals);
     H.Tconst = 0.0;
   }
-  return MC_OK;
+  return add_wells(c, H, d, 0.0);
 }
 
 // Internal numbering of a graph continuum: walk the connection graph in

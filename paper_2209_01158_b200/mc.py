@@ -42,7 +42,8 @@ class mc_continuum_desc(C.Structure):
                 ("nx", _i32), ("ny", _i32), ("h", _d), ("bc_left", _i32), ("bc_right", _i32),
                 ("g_left", _d), ("g_right", _d),
                 ("measure", _pd), ("measure_const", _d), ("n_edges", _i64), ("edge_i", _pi),
-                ("edge_j", _pi), ("edge_t", _pd), ("edge_geom", _d), ("dirichlet", _pd), ("rtol", _d)]
+                ("edge_j", _pi), ("edge_t", _pd), ("edge_geom", _d), ("dirichlet", _pd), ("rtol", _d),
+                ("well_q", _pd), ("well_p", _d)]
 
 
 class mc_coupling_desc(C.Structure):
@@ -219,6 +220,12 @@ class Problem:
                     d.edge_i = _ptr(self._arr(e[:, 0], np.int32), _pi)
                     d.edge_j = _ptr(self._arr(e[:, 1], np.int32), _pi)
                     d.edge_geom = 1.0 / h                    # |E|/d, |E| = 1, d = h (reading C7)
+                if "well_q" in c:                            # wells, paper analogue
+                    d.well_q = _ptr(self._arr(c["well_q"], np.float64))
+                    d.well_p = float(c["well_p"])
+                if c.get("u0", 0.0) != 0.0:
+                    nn = d.n
+                    d.u0 = _ptr(self._arr(np.full(nn, float(c["u0"])), np.float64))
                 conts.append(d)
             for cp in scn["couplings"]:
                 d = mc_coupling_desc(a=cp["a"], b=cp["b"])

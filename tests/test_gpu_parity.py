@@ -10,7 +10,7 @@ import math
 import numpy as np
 import pytest
 
-from inputs import CONFIGS, crop_fine, make, make_fine, make_nlmc
+from inputs import CONFIGS, crop_fine, make, make_fine, make_nlmc, make_paper_analogue
 from oracle import assemble as asm
 from oracle import schemes
 
@@ -364,3 +364,30 @@ def test_config4_cropped_standin(torch_cuda, scheme):
     got, _ = gpu_traj(scn, scheme, 4, rtols=CONFIG_RTOL[4])
     ref = oracle_traj(scn, scheme, 4)
     assert_parity(got, ref)
+
+
+# ---------------------------------------------------------------- paper analogue with wells
+@pytest.mark.parametrize("kind", ["2C", "3C"])
+@pytest.mark.parametrize("scheme", ["coupled", "D", "L", "U"])
+def test_paper_analogue_full_trajectory(torch_cuda, kind, scheme):
+    """Neumann boundaries, u0 = 1, injection wells on the fracture continuum, k_f = 1e6:
+    all 50 steps of every scheme against the oracle."""
+    scn = make_paper_analogue(kind)
+    got, reps = gpu_traj(scn, scheme, scn["NT"])
+    assert_parity(got, oracle_traj(scn, scheme, scn["NT"]))
+    assert all(r["status"] == 0 for r in reps)
+
+
+def test_wells_on_grid_continuum_ragged(torch_cuda):
+    """Well term on a grid continuum (measure h^2) and on a ragged fracture, mixed signs of
+    p_w - p, Dirichlet boundary kept: D and coupled against the oracle."""
+    scn = make_fine(37, seed=5, T=1e-2, NT=4, segments=4, lengths=(5, 20))
+    rng = np.random.default_rng(3)
+    m, f = scn["continua"]
+    m["well_q"] = np.where(rng.random(37 * 37) < 0.05, 50.0, 0.0)
+    m["well_p"] = -0.5
+    f["well_q"] = np.where(rng.random(len(scn["fracture"]["cells"])) < 0.2, 1e3, 0.0)
+    f["well_p"] = 2.0
+    for scheme in ("D", "coupled", "U"):
+        got, _ = gpu_traj(scn, scheme, 4)
+        assert_parity(got, oracle_traj(scn, scheme, 4))

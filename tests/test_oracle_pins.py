@@ -623,3 +623,49 @@ def test_U_more_accurate_than_D_paper_pattern():
     uc = schemes.run(sys_, "coupled", T / NT, NT)[-1]
     e = {k: rel(schemes.run(sys_, k, T / NT, NT, order_by_k=[0, 1])[-1], uc) for k in ("D", "L", "U")}
     assert e["U"] < e["D"], e
+
+
+# ---------------------------------------------------------------- wells (paper analogue)
+def test_wells_bruteforce_and_mass_balance():
+    """Well term f = q_w (p_w - p) on fracture cells (SPEC.md:154 sign): a literal dense
+    re-assembly adds q_w |iota| to the diagonal and q_w p_w |iota| to F; the discrete mass
+    balance then reads sum m du = tau sum_wells q_w |iota| (p_w - p^n) (coupled, Neumann)."""
+    from inputs import make_paper_analogue
+    scn = make_paper_analogue("2C", n=8, seed=3, segments=3, lengths=(3, 6), NT=5)
+    fr = scn["continua"][1]
+    fr["well_q"] = np.zeros(len(scn["fracture"]["cells"]))
+    fr["well_q"][:2] = 1e3
+    off, A, M, F = dense_fine_bruteforce(dict(scn, continua=[dict(c, dirichlet=None) for c in scn["continua"]]))
+    h = scn["h"]
+    for l in range(2):
+        A[off[1] + l, off[1] + l] += 1e3 * h
+        F[off[1] + l] += 1e3 * h * 1.2
+    sys_ = asm.assemble(scn)
+    assert np.allclose(sys_.A.toarray(), A, rtol=1e-14, atol=1e-10)
+    assert np.allclose(sys_.F, F, rtol=1e-15, atol=0)
+    tau = scn["T"] / scn["NT"]
+    u0 = sys_.u0.copy()
+    assert np.all(u0 == 1.0)
+    ref = dense_steps(off, A, M, F, tau, u0, 5, "coupled")
+    got = schemes.run(sys_, "coupled", tau, 5)
+    for r, g in zip(ref, got):   # dense LU in fp64 on a k_f = 1e6 system: cond * eps ~ 1e-12
+        assert rel(g, r) <= 1e-10
+    prev = u0
+    for u in got:
+        inflow = np.sum(1e3 * h * (1.2 - u[off[1]:off[1] + 2]))
+        assert abs(np.sum(M * (u - prev)) - tau * inflow) <= 1e-9 * tau * abs(inflow)
+        prev = u
+
+
+def test_paper_analogue_table_shape():
+    """PAPER.md Tables 1-2 / Fig. 4 pattern on the synthetic paper-analogue 2C problem:
+    every decoupled scheme within 1 % of the coupled solution at T, U-scheme the most
+    accurate (PAPER.md:956, 1139)."""
+    from inputs import make_paper_analogue
+    scn = make_paper_analogue("2C")
+    sys_ = asm.assemble(scn)
+    tau = scn["T"] / scn["NT"]
+    uc = schemes.run(sys_, "coupled", tau, scn["NT"])[-1]
+    e = {k: 100 * rel(schemes.run(sys_, k, tau, scn["NT"], order_by_k=[0, 1])[-1], uc) for k in ("L", "D", "U")}
+    assert all(v < 1.0 for v in e.values()), e
+    assert e["U"] < e["D"] and e["U"] < e["L"], e
