@@ -15,6 +15,9 @@ constexpr int kWarps = kThreads / 32;
 #ifndef MC_STAGES
 #define MC_STAGES 2
 #endif
+#ifndef MC_PROF
+#define MC_PROF 0                          // dev: per-phase clock64 instrumentation (mc_prof_read)
+#endif
 #ifndef MC_TMA
 #define MC_TMA 1                           // stage with TMA bulk copies (1) or per-lane cp.async (0)
 #endif

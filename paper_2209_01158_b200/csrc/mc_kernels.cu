@@ -62,6 +62,17 @@ __device__ __forceinline__ double pnew(double ro, double qo, double po, double d
   return __fma_rn(di, rn, __dmul_rn(b, po));
 }
 
+#if MC_PROF
+// dev instrumentation (-DMC_PROF=1 builds only): clock64 per phase of the CG loop,
+// summed over iterations by thread 0 of each group's first CTA
+__device__ long long g_prof[MC_MAX_CONTINUA][8];
+#define PROF_T(v) long long v = clock64()
+#define PROF_ADD(g, k, d) atomicAdd((unsigned long long*)&g_prof[g][k], (unsigned long long)(d))
+#else
+#define PROF_T(v)
+#define PROF_ADD(g, k, d)
+#endif
+
 struct Ctx {
   const StepParams* P;
   const double* rs;
@@ -514,11 +525,8 @@ __device__ void iter_grid2s(const Ctx& c, const ContDev& C, int x0, int y0, int 
 // Neighbours in another chunk were (or are about to be) streamed by another warp of
 // the sweep, so the far gathers hit L2.
 struct FarG {
-  double w0, w1;   // p_j of the (at most 2) far neighbours of this lane
-  int s0, s1;      // 4*h + k slot the value belongs to, -1 = none
-  int more;        // warp-uniform: some lane has > 2 far neighbours in this chunk
-  __device__ __forceinline__ double v0(const Ctx&) const { return w0; }
-  __device__ __forceinline__ double v1(const Ctx&) const { return w1; }
+  double w0, w1, w2, w3;   // p_j of the (at most 4) far neighbours of this lane, in (h, k) order
+  int s0, s1, s2, s3;      // 4*h + k slot each value belongs to, -1 = none
 };
 
 __device__ __forceinline__ void ell_codes(const double* sl, int lane, int32_t (&j)[2][4]) {
@@ -529,12 +537,14 @@ __device__ __forceinline__ void ell_codes(const double* sl, int lane, int32_t (&
     for (int k = 0; k < 4; ++k) j[h][k] = si[k * 64 + 2 * lane + h];
 }
 
-__device__ __forceinline__ FarG far_gather(const Ctx& c, const double* sl, int lane, int64_t g) {
+// far neighbours of this lane's two rows: up to 4 gathered in one batch, each load issued
+// only by the lanes that have that neighbour (no dummy own-row loads)
+__device__ __forceinline__ FarG far_gather(const Ctx& c, const double* sl, int lane) {
   int32_t j[2][4];
   ell_codes(sl, lane, j);
   FarG f;
-  f.s0 = f.s1 = -1;
-  int64_t i0 = g, i1 = g;
+  f.s0 = f.s1 = f.s2 = f.s3 = -1;
+  int32_t i0 = -1, i1 = -1, i2 = -1, i3 = -1;
   int nfar = 0;
 #pragma unroll
   for (int h = 0; h < 2; ++h)
@@ -547,16 +557,20 @@ __device__ __forceinline__ FarG far_gather(const Ctx& c, const double* sl, int l
         } else if (nfar == 1) {
           i1 = j[h][k];
           f.s1 = 4 * h + k;
+        } else if (nfar == 2) {
+          i2 = j[h][k];
+          f.s2 = 4 * h + k;
+        } else if (nfar == 3) {
+          i3 = j[h][k];
+          f.s3 = 4 * h + k;
         }
         ++nfar;
       }
-  const unsigned wfar = __reduce_max_sync(0xffffffffu, (unsigned)nfar);
-  f.more = wfar > 2;
-  f.w0 = f.w1 = 0.0;
-  if (wfar > 0) {
-    f.w0 = c.pn_at(i0);
-    f.w1 = c.pn_at(i1);
-  }
+  f.w0 = f.w1 = f.w2 = f.w3 = 0.0;
+  if (i0 >= 0) f.w0 = c.pn_at(i0);
+  if (i1 >= 0) f.w1 = c.pn_at(i1);
+  if (i2 >= 0) f.w2 = c.pn_at(i2);
+  if (i3 >= 0) f.w3 = c.pn_at(i3);
   return f;
 }
 
@@ -600,7 +614,7 @@ __device__ void iter_ells(const Ctx& c, const ContDev& C, int wg, int W, const S
   for (int m = wg; m < nch; m += W) {
     if (m + W < nch) prefetch(m + W);                             // next chunk in flight
     st.wait(tix(m));
-    const FarG fcur = far_gather(c, slot(m), lane, off + 64 * (int64_t)m + 2 * lane);
+    const FarG fcur = far_gather(c, slot(m), lane);
     // stage C: chunk m
     const double* sl = slot(m);
     const int base = 64 * m + 2 * lane;
@@ -648,9 +662,11 @@ __device__ void iter_ells(const Ctx& c, const ContDev& C, int wg, int W, const S
         double v = pc[h];                                          // -1: no neighbour
         if (cd <= -2) v = pnb[-2 - cd];
         else if (cd >= 0) {
-          if (fcur.s0 == 4 * h + k) v = fcur.v0(c);
-          else if (fcur.s1 == 4 * h + k) v = fcur.v1(c);
-          else v = c.pn_at(cd);                                    // rare: > 2 far in this lane
+          if (fcur.s0 == 4 * h + k) v = fcur.w0;
+          else if (fcur.s1 == 4 * h + k) v = fcur.w1;
+          else if (fcur.s2 == 4 * h + k) v = fcur.w2;
+          else if (fcur.s3 == 4 * h + k) v = fcur.w3;
+          else v = c.pn_at(cd);                                    // rare: > 4 far in this lane
         }
         s += pc[h] - v;
       }
@@ -1043,6 +1059,7 @@ __device__ __forceinline__ void group_allreduce(const StepParams& P, int g, int 
   }
   __syncthreads();
   double* part = P.partials + (size_t)(epoch & 1ull) * kNPart * P.total_ctas;
+  PROF_T(ta);
   if (threadIdx.x == 0) {
 #pragma unroll
     for (int k = 0; k < NP; ++k) {
@@ -1054,11 +1071,20 @@ __device__ __forceinline__ void group_allreduce(const StepParams& P, int g, int 
     // release: this CTA's r/p/q stores (ordered before by bar.sync) and its partials
     unsigned long long* ctr = &P.sync->arrive[g * kCtrStride];
     red_release_add(ctr, 1ull);
+    PROF_T(tb);
     const unsigned long long target = (epoch + 1ull) * (unsigned long long)G;
     while (ld_acquire(ctr) < target) {
     }
+#if MC_PROF
+    if (cl == 0) {
+      PROF_T(tc);
+      PROF_ADD(g, 1, tb - ta);
+      PROF_ADD(g, 2, tc - tb);
+    }
+#endif
   }
   __syncthreads();
+  PROF_T(td);
   if (w < NP) {
     double s = 0.0;
     const double* src = part + (size_t)w * P.total_ctas + base;
@@ -1071,6 +1097,12 @@ __device__ __forceinline__ void group_allreduce(const StepParams& P, int g, int 
 #pragma unroll
   for (int k = 0; k < NP; ++k) out[k] = tot[k];
   __syncthreads();
+#if MC_PROF
+  if (cl == 0 && threadIdx.x == 0) {
+    PROF_T(te);
+    PROF_ADD(g, 3, te - td);
+  }
+#endif
   ++epoch;
 }
 
@@ -1133,6 +1165,7 @@ __device__ void run_group(const StepParams& P, int g, int cl, double* x, const d
       c.pd = P.p[s ^ 1];
       c.qd = P.q[s ^ 1];
       double a5[kNPart] = {0.0, 0.0, 0.0, 0.0, 0.0};
+      PROF_T(tp0);
       for (int k = 0; k < P.L; ++k)
         if (((G.cont_mask >> k) & 1) && P.cont[k].rr) {
           if (P.cont[k].resident) iter_ells_res<CPL>(c, P.cont[k], wg, W, st, j == 0, a5);
@@ -1151,6 +1184,13 @@ __device__ void run_group(const StepParams& P, int g, int cl, double* x, const d
         }
       }
       double t5[kNPart];
+#if MC_PROF
+      if (cl == 0 && threadIdx.x == 0) {
+        PROF_T(tp1);
+        PROF_ADD(g, 0, tp1 - tp0);
+        PROF_ADD(g, 4, 1);
+      }
+#endif
       group_allreduce<kNPart>(P, g, cl, epoch, a5, t5);
       passes = j + 1;
       rr = t5[1];
@@ -1314,6 +1354,17 @@ cudaError_t launch_step(const StepParams* params, int total_ctas, cudaStream_t s
   return cudaLaunchCooperativeKernel((const void*)step_kernel, dim3(total_ctas), dim3(kThreads),
                                      args, kDynSmem, s);
 }
+
+#if MC_PROF
+extern "C" int mc_prof_read(long long* out, int reset) {
+  cudaError_t e = cudaMemcpyFromSymbol(out, g_prof, sizeof(g_prof));
+  if (reset) {
+    static long long z[MC_MAX_CONTINUA][8] = {};
+    cudaMemcpyToSymbol(g_prof, z, sizeof(z));
+  }
+  return (int)e;
+}
+#endif
 
 cudaError_t step_kernel_occupancy(int* blocks_per_sm) {
   cudaError_t e = cudaFuncSetAttribute((const void*)step_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kDynSmem);
