@@ -39,7 +39,7 @@
 extern "C" {
 #endif
 
-#define MC_ABI_VERSION 1
+#define MC_ABI_VERSION 2
 #define MC_MAX_CONTINUA 4
 
 typedef struct mc_ctx mc_ctx;
@@ -130,6 +130,11 @@ typedef struct {
                                                     q_w|cell| on the diagonal and
                                                     q_w p_w |cell| in F                     */
   double well_p;                                 /* p_w                                    */
+  /* since ABI 2 — general symmetric operators such as the NLMC coarse system
+     (PAPER.md:667-729), whose transmissibilities may have either sign: */
+  const double* diag_extra;                      /* MC_GRAPH: NULL, or per cell a term added
+                                                    to the diagonal of A (any sign)          */
+  int32_t signed_edges;                          /* MC_GRAPH: 1 = edge_t may be negative    */
 } mc_continuum_desc;
 
 /*
@@ -149,6 +154,8 @@ typedef struct {
   const int32_t* j_b;
   const double* sigma;  double sigma_const;     /* sigma >= 0                             */
   int32_t scale_by_measure;
+  int32_t signed_sigma;                          /* since ABI 2: 1 = sigma may be negative
+                                                    (NLMC between-continuum entries)        */
 } mc_coupling_desc;
 
 /* Per-step report.  For MC_COUPLED there is one solve (nsolves = 1, index 0). */
@@ -211,6 +218,65 @@ mc_status mc_destroy(mc_ctx* ctx);
 const char* mc_error_string(const mc_ctx* ctx);
 
 int32_t mc_abi_version(void);
+
+/* ------------------------------------------------------------------------------------
+ * NLMC multiscale space (§4.1, :591-729).
+ *
+ * Coarse cells K_j: the fine grid continua (all MC_GRID2D continua of the context share
+ * one nx x ny grid) split into nHx x nHy blocks; K_j^alpha = the cells of continuum
+ * alpha in K_j.  A graph continuum's cell belongs to the block of its host grid cell
+ * (host[alpha][cell] = iy*nx + ix); every connected piece of a graph continuum inside
+ * one block is its own coarse DOF (reading C30).  K_i^+ = K_i plus `oversample` block
+ * layers, clipped.
+ *
+ * For every coarse cell i and every coarse DOF (i, beta) the basis psi^{i,beta} solves
+ * Eq. eq:basis: the fine coupled operator D + Q on the cells of K_i^+
+ * (zero Dirichlet outside) with the coarse-mean constraints
+ * (1/|K_j^alpha|) int psi_alpha = delta_ij delta_alpha beta.  On the
+ * GPU: one CTA per K_i^+, banded Cholesky of D + Q in a bandwidth-minimising order, the
+ * Schur complement C (D+Q)^{-1} C^T, its dense Cholesky, psi = (D+Q)^{-1} C^T S^{-1} e.
+ * Coarse system (Eq. app-nlmc): Abar = Dbar + Qbar + Wbar with Dbar = R D R^T in flux
+ * form (reading C32), Qbar, Wbar (well terms), Mbar, Fbar aggregated over K_j^alpha
+ * (reading C31); u0bar = measure-weighted means.
+ *
+ * The fine context must have its continua and couplings set and no step taken yet (the
+ * build reads the setup data); it is unchanged by the build.  Graph continua with fixed
+ * (Dirichlet) cells are not supported (MC_ERR_ARG).  A K_i^+ whose restricted operator
+ * is singular (pure no-flow, K_i^+ = whole domain, no transfer sink) fails with
+ * MC_ERR_ARG naming i.
+ */
+typedef struct mc_nlmc mc_nlmc;
+
+typedef struct {
+  int32_t nHx, nHy;                              /* coarse blocks; nx % nHx == ny % nHy == 0 */
+  int32_t oversample;                            /* m >= 0 block layers                      */
+  const int32_t* host[MC_MAX_CONTINUA];          /* MC_GRAPH continua: host grid cell of each
+                                                    cell (host or device); NULL for grids    */
+} mc_nlmc_desc;
+
+mc_status mc_nlmc_build(mc_ctx* fine, const mc_nlmc_desc* desc, mc_nlmc** out);
+
+/* Sizes: coarse DOFs per continuum (n_alpha[MC_MAX_CONTINUA], unused = 0), Abar nonzeros,
+ * fine DOFs.  Coarse DOFs are numbered continuum-major, then by coarse cell, then piece. */
+mc_status mc_nlmc_sizes(const mc_nlmc* nl, int64_t* n_alpha, int64_t* nnz, int64_t* n_fine);
+
+/* Coarse system, host or device output arrays: Abar in CSR (rowptr[n+1], col[nnz],
+ * val[nnz], rows sorted by column), Mbar[n], Fbar[n], u0bar[n]; key[3n] = (continuum,
+ * coarse cell, piece) of each coarse DOF; fine_dof[n_fine] = coarse DOF of each fine
+ * DOF (fine DOFs: the context's continua concatenated in caller numbering).  Any
+ * output pointer may be NULL. */
+mc_status mc_nlmc_get(const mc_nlmc* nl, int32_t* rowptr, int32_t* col, double* val, double* mass,
+                      double* rhs, double* u0, int32_t* key, int32_t* fine_dof);
+
+/* Basis psi^{r} of coarse DOF r as a fine vector (n_fine doubles, zero outside K_i^+). */
+mc_status mc_nlmc_basis(const mc_nlmc* nl, int64_t r, double* psi);
+
+/* Device time (ms) of the basis kernel and of the projection kernel of the build. */
+mc_status mc_nlmc_times(const mc_nlmc* nl, double* ms_basis, double* ms_project);
+
+const char* mc_nlmc_error_string(const mc_nlmc* nl);
+mc_status mc_nlmc_destroy(mc_nlmc* nl);
+
 
 #ifdef __cplusplus
 }

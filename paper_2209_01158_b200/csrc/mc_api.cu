@@ -15,6 +15,7 @@
 #include <vector>
 
 #include "mc_internal.h"
+#include "mc_nlmc.h"
 
 using namespace mc;
 
@@ -29,6 +30,7 @@ struct HostCont {
   int32_t nx = 0, ny = 0;
   double h = 0.0;
   std::vector<double> mtau, dbase, F, u0, tsum, measure;
+  std::vector<double> mass, dbd, dwell;        // m = c|cell|; non-edge diagonal of D; well terms (NLMC)
   std::vector<double> Tx, Ty;                  // grid
   std::vector<int32_t> rowptr, col;            // graph, local columns
   std::vector<double> val;                     // graph per-entry T (empty -> uniform)
@@ -261,6 +263,7 @@ static mc_status add_wells(mc_ctx* c, HostCont& H, const mc_continuum_desc* d, d
     if (!H.fixed.empty() && H.fixed[s]) continue;
     const double w = q[s] * (meas_const > 0.0 ? meas_const : H.measure[s]);
     H.dbase[s] += w;
+    H.dwell[s] += w;
     H.F[s] += w * d->well_p;
   }
   return MC_OK;
@@ -298,6 +301,9 @@ static mc_status set_grid(mc_ctx* c, HostCont& H, const mc_continuum_desc* d) {
   H.dbase.resize((size_t)n);
   H.F.assign((size_t)n, 0.0);
   H.measure.assign((size_t)n, area);
+  H.mass.assign((size_t)n, 0.0);
+  H.dbd.assign((size_t)n, 0.0);
+  H.dwell.assign((size_t)n, 0.0);
   const bool kc = (d->k == nullptr);
   // T = k |E|/d, |E| = d = h; harmonic mean for a k field (reading C2)
   for (int iy = 0; iy < ny; ++iy)
@@ -329,6 +335,8 @@ static mc_status set_grid(mc_ctx* c, HostCont& H, const mc_continuum_desc* d) {
       }
       H.dbase[i] = H.mtau[i] + db;
       H.F[i] = Fi;
+      H.mass[i] = m;
+      H.dbd[i] = db;
     }
   return add_wells(c, H, d, area);
 }
@@ -369,8 +377,9 @@ static mc_status set_graph(mc_ctx* c, HostCont& H, const mc_continuum_desc* d) {
     if (a < 0 || b < 0 || a >= n || b >= n || a == b)
       return fail(c, MC_ERR_ARG, "edge %lld = (%d, %d) out of range or self-loop", (long long)e, a, b);
     key[(size_t)e] = (int64_t)std::min(a, b) * n + std::max(a, b);
-    if (d->edge_t && !finite_nonneg(et[(size_t)e]))
-      return fail(c, MC_ERR_ARG, "edge_t[%lld] = %g must be finite and >= 0", (long long)e, et[(size_t)e]);
+    if (d->edge_t && !(d->signed_edges ? std::isfinite(et[(size_t)e]) : finite_nonneg(et[(size_t)e])))
+      return fail(c, MC_ERR_ARG, "edge_t[%lld] = %g must be finite%s", (long long)e, et[(size_t)e],
+                  d->signed_edges ? "" : " and >= 0");
   }
   {
     std::vector<int64_t> ks(key);
@@ -387,15 +396,30 @@ static mc_status set_graph(mc_ctx* c, HostCont& H, const mc_continuum_desc* d) {
   H.tsum.assign((size_t)n, 0.0);
   H.fixed.assign((size_t)n, 0);
   H.gfix.assign((size_t)n, 0.0);
+  H.mass.assign((size_t)n, 0.0);
+  H.dbd.assign((size_t)n, 0.0);
+  H.dwell.assign((size_t)n, 0.0);
+  std::vector<double> dx;
+  if (d->diag_extra) {
+    if ((st = fetch(c, dx, d->diag_extra, n)) != MC_OK) return st;
+    for (double v : dx)
+      if (!std::isfinite(v)) return fail(c, MC_ERR_ARG, "diag_extra not finite");
+  }
   for (int64_t i = 0; i < n; ++i) {
     const size_t s = (size_t)i;
+    H.mass[s] = cc[s] * meas[s];
     H.mtau[s] = cc[s] * meas[s] / tau;                       // m = c |cell|
     H.dbase[s] = H.mtau[s];
+    if (!dx.empty()) {                                       // explicit diagonal term (ABI 2)
+      H.dbase[s] += dx[s];
+      H.dbd[s] += dx[s];
+    }
     H.F[s] = f.empty() ? 0.0 : f[s] * meas[s];
     if (!dir.empty() && !std::isnan(dir[s])) {                // fixed DOF: identity row (C12)
       H.fixed[s] = 1;
       H.gfix[s] = dir[s];
       H.mtau[s] = 0.0;
+      H.mass[s] = 0.0;
       H.dbase[s] = 1.0;
       H.F[s] = dir[s];
     }
@@ -418,9 +442,11 @@ static mc_status set_graph(mc_ctx* c, HostCont& H, const mc_continuum_desc* d) {
       cnt[(size_t)b + 1]++;
     } else if (!fa && fb) {
       H.dbase[(size_t)a] += T[(size_t)e];
+      H.dbd[(size_t)a] += T[(size_t)e];
       H.F[(size_t)a] += T[(size_t)e] * H.gfix[(size_t)b];
     } else if (fa && !fb) {
       H.dbase[(size_t)b] += T[(size_t)e];
+      H.dbd[(size_t)b] += T[(size_t)e];
       H.F[(size_t)b] += T[(size_t)e] * H.gfix[(size_t)a];
     }
   }
@@ -511,6 +537,9 @@ static void apply_chain_order(HostCont& H) {
   };
   pv(H.mtau);
   pv(H.dbase);
+  pv(H.mass);
+  pv(H.dbd);
+  pv(H.dwell);
   pv(H.F);
   pv(H.u0);
   pv(H.tsum);
@@ -614,7 +643,17 @@ extern "C" mc_status mc_set_coupling(mc_ctx* c, const mc_coupling_desc* d) {
     hcp.j.resize((size_t)m);
     std::iota(hcp.j.begin(), hcp.j.end(), 0);
   }
-  if ((st = field(c, hcp.s, d->sigma, d->sigma_const, m, "sigma", false)) != MC_OK) return st;
+  if (d->signed_sigma) {                                    // ABI 2: any finite sigma (NLMC)
+    if (d->sigma) {
+      if ((st = fetch(c, hcp.s, d->sigma, m)) != MC_OK) return st;
+    } else {
+      hcp.s.assign((size_t)m, d->sigma_const);
+    }
+    for (double v : hcp.s)
+      if (!std::isfinite(v)) return fail(c, MC_ERR_ARG, "sigma not finite");
+  } else if ((st = field(c, hcp.s, d->sigma, d->sigma_const, m, "sigma", false)) != MC_OK) {
+    return st;
+  }
   for (int64_t e = 0; e < m; ++e) {
     const int32_t i = hcp.i[(size_t)e], j = hcp.j[(size_t)e];
     if (i < 0 || i >= A.n || j < 0 || j >= B.n)
@@ -1213,3 +1252,106 @@ extern "C" mc_status mc_last_kernel_ms(mc_ctx* c, double* ms_out) {
   *ms_out = ms;
   return MC_OK;
 }
+
+// ====================================================================== NLMC export
+namespace mc {
+
+mc_status ctx_error(mc_ctx* c, mc_status st, const char* msg) { return fail(c, st, "%s", msg); }
+
+mc_status export_fine(mc_ctx* c, const int32_t* const* host, FineSystem& fs) {
+  if (!c) return MC_ERR_ARG;
+  if (c->finalized) return fail(c, MC_ERR_STATE, "NLMC build after the first step (setup data released)");
+  fs = FineSystem();
+  fs.L = c->L;
+  fs.off.assign((size_t)c->L + 1, 0);
+  for (int a = 0; a < c->L; ++a) {
+    const HostCont& H = c->hc[a];
+    if (!H.set) return fail(c, MC_ERR_STATE, "continuum %d not set", a);
+    fs.off[(size_t)a + 1] = fs.off[(size_t)a] + H.n;
+    fs.kind.push_back(H.kind);
+    if (H.kind == KIND_GRID) {
+      if (fs.nx == 0) {
+        fs.nx = H.nx;
+        fs.ny = H.ny;
+      } else if (fs.nx != H.nx || fs.ny != H.ny) {
+        return fail(c, MC_ERR_ARG, "NLMC: grid continua on different grids");
+      }
+    } else {
+      for (uint8_t f : H.fixed)
+        if (f) return fail(c, MC_ERR_ARG, "NLMC: continuum %d has fixed (Dirichlet) cells", a);
+    }
+  }
+  if (fs.nx == 0) return fail(c, MC_ERR_ARG, "NLMC needs a grid continuum");
+  const int64_t N = fs.off[(size_t)c->L];
+  fs.cont.resize((size_t)N);
+  fs.host.resize((size_t)N);
+  fs.meas.resize((size_t)N);
+  fs.mass.resize((size_t)N);
+  fs.F.resize((size_t)N);
+  fs.u0.resize((size_t)N);
+  fs.ddiag.resize((size_t)N);
+  fs.wdiag.resize((size_t)N);
+  auto caller = [&](int a, int64_t t) -> int64_t {      // internal position -> caller index
+    const HostCont& H = c->hc[a];
+    return H.perm.empty() ? t : (int64_t)H.perm[(size_t)t];
+  };
+  for (int a = 0; a < c->L; ++a) {
+    const HostCont& H = c->hc[a];
+    const int64_t o = fs.off[(size_t)a];
+    std::vector<int32_t> hc;
+    if (H.kind == KIND_GRAPH) {
+      if (!host || !host[a]) return fail(c, MC_ERR_ARG, "NLMC: host cells of graph continuum %d missing", a);
+      mc_status st = fetch(c, hc, host[a], H.n);
+      if (st != MC_OK) return st;
+      for (int32_t v : hc)
+        if (v < 0 || (int64_t)v >= (int64_t)fs.nx * fs.ny)
+          return fail(c, MC_ERR_ARG, "NLMC: host cell %d of continuum %d out of range", v, a);
+    }
+    for (int64_t t = 0; t < H.n; ++t) {
+      const int64_t i = caller(a, t);
+      const size_t g = (size_t)(o + i);
+      fs.cont[g] = a;
+      fs.host[g] = H.kind == KIND_GRID ? (int32_t)i : hc[(size_t)i];
+      fs.meas[g] = H.measure[(size_t)t];
+      fs.mass[g] = H.mass[(size_t)t];
+      fs.F[g] = H.F[(size_t)t];
+      fs.u0[g] = H.u0[(size_t)t];
+      fs.ddiag[g] = H.dbd[(size_t)t];
+      fs.wdiag[g] = H.dwell[(size_t)t];
+    }
+    if (H.kind == KIND_GRID) {
+      for (int iy = 0; iy < H.ny; ++iy)
+        for (int ix = 0; ix < H.nx; ++ix) {
+          const int64_t i = (int64_t)iy * H.nx + ix;
+          if (ix + 1 < H.nx && H.Tx[(size_t)i] != 0.0) {
+            fs.ei.push_back((int32_t)(o + i));
+            fs.ej.push_back((int32_t)(o + i + 1));
+            fs.et.push_back(H.Tx[(size_t)i]);
+          }
+          if (iy + 1 < H.ny && H.Ty[(size_t)i] != 0.0) {
+            fs.ei.push_back((int32_t)(o + i));
+            fs.ej.push_back((int32_t)(o + i + H.nx));
+            fs.et.push_back(H.Ty[(size_t)i]);
+          }
+        }
+    } else {
+      for (int64_t t = 0; t < H.n; ++t)
+        for (int32_t e = H.rowptr[(size_t)t]; e < H.rowptr[(size_t)t + 1]; ++e) {
+          const int32_t u = H.col[(size_t)e];
+          if (u <= t) continue;                               // each connection once
+          fs.ei.push_back((int32_t)(o + caller(a, t)));
+          fs.ej.push_back((int32_t)(o + caller(a, u)));
+          fs.et.push_back(H.val.empty() ? H.Tconst : H.val[(size_t)e]);
+        }
+    }
+  }
+  for (const HostCoupling& h : c->cpl)
+    for (size_t e = 0; e < h.i.size(); ++e) {
+      fs.qi.push_back((int32_t)(fs.off[(size_t)h.a] + caller(h.a, h.i[e])));
+      fs.qj.push_back((int32_t)(fs.off[(size_t)h.b] + caller(h.b, h.j[e])));
+      fs.qs.push_back(h.s[e]);
+    }
+  return MC_OK;
+}
+
+}  // namespace mc

@@ -43,12 +43,16 @@ class mc_continuum_desc(C.Structure):
                 ("g_left", _d), ("g_right", _d),
                 ("measure", _pd), ("measure_const", _d), ("n_edges", _i64), ("edge_i", _pi),
                 ("edge_j", _pi), ("edge_t", _pd), ("edge_geom", _d), ("dirichlet", _pd), ("rtol", _d),
-                ("well_q", _pd), ("well_p", _d)]
+                ("well_q", _pd), ("well_p", _d), ("diag_extra", _pd), ("signed_edges", _i32)]
 
 
 class mc_coupling_desc(C.Structure):
     _fields_ = [("a", _i32), ("b", _i32), ("nnz", _i64), ("i_a", _pi), ("j_b", _pi), ("sigma", _pd),
-                ("sigma_const", _d), ("scale_by_measure", _i32)]
+                ("sigma_const", _d), ("scale_by_measure", _i32), ("signed_sigma", _i32)]
+
+
+class mc_nlmc_desc(C.Structure):
+    _fields_ = [("nHx", _i32), ("nHy", _i32), ("oversample", _i32), ("host", C.c_void_p * MC_MAX_CONTINUA)]
 
 
 class mc_step_report(C.Structure):
@@ -67,7 +71,8 @@ class mc_step_report(C.Structure):
 EXPORTS = ["mc_create", "mc_set_continuum", "mc_set_coupling", "mc_step_decoupled", "mc_step_coupled",
            "mc_step", "mc_set_permeability_order",
            "mc_run", "mc_get_state", "mc_set_state", "mc_size", "mc_last_kernel_ms", "mc_destroy",
-           "mc_error_string", "mc_abi_version"]
+           "mc_error_string", "mc_abi_version", "mc_nlmc_build", "mc_nlmc_sizes", "mc_nlmc_get",
+           "mc_nlmc_basis", "mc_nlmc_times", "mc_nlmc_error_string", "mc_nlmc_destroy"]
 
 _lib = None
 
@@ -100,8 +105,16 @@ def load(path: str | None = None):
     lib.mc_error_string.argtypes = [P]
     lib.mc_error_string.restype = C.c_char_p
     lib.mc_abi_version.restype = _i32
+    lib.mc_nlmc_build.argtypes = [P, C.POINTER(mc_nlmc_desc), C.POINTER(P)]
+    lib.mc_nlmc_sizes.argtypes = [P, C.POINTER(_i64), C.POINTER(_i64), C.POINTER(_i64)]
+    lib.mc_nlmc_get.argtypes = [P] + [P] * 8
+    lib.mc_nlmc_basis.argtypes = [P, _i64, P]
+    lib.mc_nlmc_times.argtypes = [P, _pd, _pd]
+    lib.mc_nlmc_error_string.argtypes = [P]
+    lib.mc_nlmc_error_string.restype = C.c_char_p
+    lib.mc_nlmc_destroy.argtypes = [P]
     for name in EXPORTS:
-        if name != "mc_size" and name != "mc_error_string" and name != "mc_abi_version":
+        if name not in ("mc_size", "mc_error_string", "mc_abi_version", "mc_nlmc_error_string"):
             getattr(lib, name).restype = _i32
     _lib = lib
     return lib
@@ -118,6 +131,8 @@ def permeability_order(scn):
     """Continuum ids by ascending permeability: the scenario's k
     (geometric mean of a k field), the fracture's k_f, NLMC k_scale (marshalling of a
     physical description, the order itself is a caller input of the ABI)."""
+    if "korder" in scn:
+        return list(scn["korder"])
     if scn["kind"] == "fine":
         ks = []
         for c in scn["continua"]:
@@ -258,9 +273,38 @@ class Problem:
             d.j_b = _ptr(self._arr(bj, np.int32), _pi)
             d.sigma = _ptr(self._arr(bt, np.float64))
             cpls.append(d)
+        elif scn["kind"] == "coarse":
+            # an assembled symmetric coarse system (NLMC, NlmcSpace.coarse_scenario): every
+            # off-diagonal entry a_ij becomes a signed transmissibility / transfer -a_ij, the
+            # row sums go to diag_extra, so the library's diagonal is exactly a_ii (C32)
+            for blk in scn["blocks"]:
+                d = mc_continuum_desc(kind=MC_GRAPH, n=blk["n"])
+                d.c = _ptr(self._arr(blk["mass"], np.float64))
+                d.measure_const = 1.0
+                d.f = _ptr(self._arr(blk["F"], np.float64))
+                d.u0 = _ptr(self._arr(blk["u0"], np.float64))
+                d.n_edges = len(blk["ei"])
+                d.edge_i = _ptr(self._arr(blk["ei"], np.int32), _pi)
+                d.edge_j = _ptr(self._arr(blk["ej"], np.int32), _pi)
+                d.edge_t = _ptr(self._arr(blk["et"], np.float64))
+                d.signed_edges = 1
+                d.diag_extra = _ptr(self._arr(blk["rowsum"], np.float64))
+                conts.append(d)
+            for cp in scn["couplings"]:
+                d = mc_coupling_desc(a=cp["a"], b=cp["b"], nnz=len(cp["i"]))
+                d.i_a = _ptr(self._arr(cp["i"], np.int32), _pi)
+                d.j_b = _ptr(self._arr(cp["j"], np.int32), _pi)
+                d.sigma = _ptr(self._arr(cp["sigma"], np.float64))
+                d.signed_sigma = 1
+                cpls.append(d)
         else:
             raise ValueError(scn["kind"])
         return conts, cpls
+
+    def nlmc(self, nHx, nHy, oversample):
+        """NLMC multiscale space of this (not yet stepped) fine problem: bases and the
+        coarse system built by the library on the GPU (mc_nlmc_build)."""
+        return NlmcSpace(self, nHx, nHy, oversample)
 
     # ------------------------------------------------------------------ calls
     def _check(self, st, create=False, report=None):
@@ -314,3 +358,98 @@ class Problem:
         except Exception:
             pass
 
+
+
+class NlmcSpace:
+    """Result of mc_nlmc_build (include/mc.h): coarse system Abar (CSR), Mbar, Fbar, u0bar,
+    coarse DOF keys (continuum, coarse cell, piece), fine -> coarse map, bases on demand."""
+
+    def __init__(self, pb: Problem, nHx, nHy, oversample):
+        self.lib, self.pb = pb.lib, pb
+        scn = pb.scn
+        d = mc_nlmc_desc(nHx=nHx, nHy=nHy, oversample=oversample)
+        hosts = []
+        for a, c in enumerate(scn["continua"]):
+            if c["kind"] != "grid":
+                h = np.ascontiguousarray(scn["fracture"]["cells"], dtype=np.int32)
+                hosts.append(h)
+                d.host[a] = h.ctypes.data_as(C.c_void_p)
+        self.h = C.c_void_p()
+        st = self.lib.mc_nlmc_build(pb.ctx, C.byref(d), C.byref(self.h))
+        pb._check(st)
+        na = (_i64 * MC_MAX_CONTINUA)()
+        nnz, nf = _i64(), _i64()
+        self.lib.mc_nlmc_sizes(self.h, na, C.byref(nnz), C.byref(nf))
+        self.L = pb.L
+        self.sizes = [int(na[a]) for a in range(self.L)]
+        n = sum(self.sizes)
+        self.n, self.nnz, self.n_fine = n, int(nnz.value), int(nf.value)
+        self.rowptr = np.zeros(n + 1, np.int32)
+        self.col = np.zeros(self.nnz, np.int32)
+        self.val = np.zeros(self.nnz)
+        self.mass, self.rhs, self.u0 = np.zeros(n), np.zeros(n), np.zeros(n)
+        self.key = np.zeros(3 * n, np.int32)
+        self.fine_dof = np.zeros(self.n_fine, np.int32)
+        arrs = [self.rowptr, self.col, self.val, self.mass, self.rhs, self.u0, self.key, self.fine_dof]
+        st = self.lib.mc_nlmc_get(self.h, *[a.ctypes.data_as(C.c_void_p) for a in arrs])
+        if st != MC_OK:
+            raise MCError(st, "mc_nlmc_get")
+        self.key = self.key.reshape(n, 3)
+        tb, tp = C.c_double(), C.c_double()
+        self.lib.mc_nlmc_times(self.h, C.byref(tb), C.byref(tp))
+        self.ms_basis, self.ms_project = tb.value, tp.value
+        self.korder = pb.korder
+
+    def basis(self, r):
+        out = np.zeros(self.n_fine)
+        st = self.lib.mc_nlmc_basis(self.h, int(r), out.ctypes.data_as(C.c_void_p))
+        if st != MC_OK:
+            raise MCError(st, "mc_nlmc_basis")
+        return out
+
+    def coarse_scenario(self, T, NT):
+        """The coarse system as a 'coarse' scenario for Problem (signed ABI-2 descriptors)."""
+        return coarse_scenario(self.rowptr, self.col, self.val, self.mass, self.rhs, self.u0, self.sizes,
+                               T, NT, self.korder)
+
+    def close(self):
+        if self.h:
+            self.lib.mc_nlmc_destroy(self.h)
+            self.h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def coarse_scenario(rowptr, col, val, mass, rhs, u0, sizes, T, NT, korder=None):
+    """An assembled symmetric system (CSR, blocks of `sizes` rows) as a 'coarse' scenario:
+    within-block off-diagonals -> signed edges, between-block -> signed transfer entries,
+    row sums -> diag_extra (marshalling for mc_set_continuum / mc_set_coupling, ABI 2)."""
+    n = int(sum(sizes))
+    off = np.concatenate([[0], np.cumsum(sizes)])
+    rowptr = np.asarray(rowptr, dtype=np.int64)
+    rows = np.repeat(np.arange(n), np.diff(rowptr))
+    cols, vals = np.asarray(col, dtype=np.int64), np.asarray(val, dtype=np.float64)
+    blk = np.searchsorted(off, rows, side="right") - 1
+    bcol = np.searchsorted(off, cols, side="right") - 1
+    rowsum = np.bincount(rows, weights=vals, minlength=n)
+    L = len(sizes)
+    blocks, cpls = [], []
+    for a in range(L):
+        sel = (blk == a) & (bcol == a) & (rows < cols)
+        lo, hi = off[a], off[a + 1]
+        blocks.append(dict(n=int(hi - lo), mass=np.asarray(mass)[lo:hi], F=np.asarray(rhs)[lo:hi],
+                           u0=np.asarray(u0)[lo:hi], ei=rows[sel] - lo, ej=cols[sel] - lo, et=-vals[sel],
+                           rowsum=rowsum[lo:hi]))
+    for a in range(L):
+        for b in range(a + 1, L):
+            sel = (blk == a) & (bcol == b)
+            if sel.any():
+                cpls.append(dict(a=a, b=b, i=rows[sel] - off[a], j=cols[sel] - off[b], sigma=-vals[sel]))
+    out = dict(kind="coarse", T=float(T), NT=int(NT), blocks=blocks, couplings=cpls)
+    if korder is not None:
+        out["korder"] = list(korder)
+    return out

@@ -28,7 +28,8 @@ def lib():
 def test_header_declares_the_boundary():
     names = _declared()
     for must in ["mc_create", "mc_set_continuum", "mc_set_coupling", "mc_step_decoupled",
-                 "mc_step_coupled", "mc_run", "mc_destroy", "mc_get_state", "mc_error_string"]:
+                 "mc_step_coupled", "mc_run", "mc_destroy", "mc_get_state", "mc_error_string",
+                 "mc_nlmc_build", "mc_nlmc_get", "mc_nlmc_basis"]:
         assert must in names
 
 
@@ -40,7 +41,7 @@ def test_library_exports_every_declared_symbol(lib):
     out = subprocess.run(["nm", "-D", "--defined-only", mc.LIB_PATH], capture_output=True, text=True).stdout
     exported = set(re.findall(r" T (mc_\w+)$", out, re.M))
     assert set(_declared()) <= exported
-    assert lib.mc_abi_version() == 1
+    assert lib.mc_abi_version() == 2
 
 
 def test_struct_layouts_match_header(tmp_path):
@@ -51,6 +52,7 @@ def test_struct_layouts_match_header(tmp_path):
         "mc_continuum_desc": [f[0] for f in mc.mc_continuum_desc._fields_],
         "mc_coupling_desc": [f[0] for f in mc.mc_coupling_desc._fields_],
         "mc_step_report": [f[0] for f in mc.mc_step_report._fields_],
+        "mc_nlmc_desc": [f[0] for f in mc.mc_nlmc_desc._fields_],
     }
     lines = ['#include <stdio.h>', '#include <stddef.h>', f'#include "{HEADER}"', "int main(void){"]
     for s, fs in fields.items():
