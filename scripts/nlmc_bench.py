@@ -21,6 +21,14 @@ args = ap.parse_args()
 rows = []
 for kind in ("2C", "3C"):
     scn = make_paper_analogue(kind)
+    # fine reference: the coupled fine solution (GPU fine path) at t = T, averaged over K_j^alpha
+    fp = Problem(scn)
+    fp.run("coupled", scn["NT"])
+    fine_T = np.concatenate([t.cpu().numpy() for t in fp.state()])
+    h = scn["h"]
+    meas = np.concatenate([np.full(fp.sizes[a], h * h if c["kind"] == "grid" else h)
+                           for a, c in enumerate(scn["continua"])])
+    fp.close()
     for nH in (20, 40):
         m = 2
         pb = Problem(scn)
@@ -31,10 +39,14 @@ for kind in ("2C", "3C"):
                    nnz_per_row=sp_.nnz / sp_.n, ms_basis_kernel=sp_.ms_basis, ms_project_kernel=sp_.ms_project,
                    s_build_wall=wall)
         cs = sp_.coarse_scenario(scn["T"], scn["NT"])
+        pbar = np.bincount(sp_.fine_dof, weights=meas * fine_T, minlength=sp_.n) / \
+            np.bincount(sp_.fine_dof, weights=meas, minlength=sp_.n)
         for scheme in ("coupled", "L", "D", "U"):
             cp = Problem(cs)
             reps = cp.run(scheme, scn["NT"])
             torch.cuda.synchronize()
+            got = np.concatenate([t.cpu().numpy() for t in cp.state()])
+            row[f"{scheme}_eH_pct"] = 100.0 * float(np.linalg.norm(got - pbar) / np.linalg.norm(pbar))
             row[f"{scheme}_ms"] = float(sum(r["ms"] for r in reps))
             row[f"{scheme}_iters_per_step"] = [float(np.mean([r["iters"][k] for r in reps]))
                                                for k in range(len(reps[0]["iters"]))]
