@@ -5,9 +5,9 @@
 // the lower band of D + Q restricted to K_i^+ (zero Dirichlet outside),
 // the constraint rows.
 // Device (sm_100a):
-//   nlmc_basis_kernel   one persistent CTA per SM, one K_i^+ at a time:
-//                       banded Cholesky D + Q = L L^T (right-looking, (b+1)^2 window in
-//                       shared memory), Z = (D+Q)^{-1} C^T by banded forward / backward
+//   nlmc_basis_kernel   one CTA per K_i^+ (persistent, as many per SM as shared memory allows):
+//                       banded Cholesky D + Q = L L^T (right-looking, ring of b+1+8 rows
+//                       in shared memory, cp.async prefetch), Z = (D+Q)^{-1} C^T by banded forward / backward
 //                       substitution for all constraint columns at once, Schur complement
 //                       S = C Z and its dense Cholesky, psi^{i,beta} = Z S^{-1} e_(i,beta)
 //                       -- Eq. eq:basis by block elimination of the multipliers.
@@ -28,10 +28,10 @@
 
 namespace mc {
 
-constexpr int kNlThreads = 512;
-constexpr int kNlMaxBand = 160;      // (b+1)^2 doubles of window in shared memory
-constexpr int kNlMaxCons = 128;      // constraint rows per K_i^+
-constexpr int kNlSmemDoubles = 27000;   // 216 KB dynamic shared memory
+constexpr int kNlThreads = 256;      // one CTA per region K_i^+
+constexpr int kWP = 8;               // cp.async prefetch distance (rows)
+constexpr int kNlMaxCons = 128;      // constraint rows per K_i^+ (4 per lane)
+constexpr int kNlSmemDoubles = 27000;   // 216 KB dynamic shared memory per CTA
 
 struct NlDomain {
   int32_t n, b, kc, nown;       // local DOFs, bandwidth, constraints, own coarse DOFs
@@ -62,41 +62,66 @@ struct NlParams {
   double* psi;                  // output
   int64_t band_stride, z_stride;
   int32_t* err;                 // first failing domain + 1 (0 = ok)
+  int32_t wpb;                  // warps per CTA
+  int32_t spw;                  // shared-memory doubles per warp
 };
 
 // ---------------------------------------------------------------- basis kernel
-__global__ void __launch_bounds__(kNlThreads, 1) nlmc_basis_kernel(const NlParams P) {
+// One WARP per region K_i^+ (a few warps per CTA, persistent over regions): no CTA
+// barriers on the sequential paths, only __syncwarp.  Global rows the next steps need are
+// prefetched kWP rows ahead with cp.async into per-warp shared-memory rings.
+__device__ __forceinline__ unsigned nl_smem(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void nl_cp8(double* dst, const double* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(nl_smem(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void nl_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void nl_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+__global__ void __launch_bounds__(kNlThreads) nlmc_basis_kernel(const NlParams P) {
   extern __shared__ __align__(16) double sm[];
   const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
-  const int nw = kNlThreads / 32;
+  constexpr int NT = kNlThreads, NW = kNlThreads / 32;
+  double* ws = sm;
   double* band = P.band + (size_t)blockIdx.x * P.band_stride;
   double* Z = P.Z + (size_t)blockIdx.x * P.z_stride;
   for (int di = blockIdx.x; di < P.ndom; di += gridDim.x) {
     const NlDomain D = P.dom[di];
-    const int n = D.n, b = D.b, kc = D.kc, bw = b + 1;
+    const int n = D.n, b = D.b, kc = D.kc, bw = b + 1, R = bw + kWP;
     const int32_t* lcon = P.lcon + D.dof0;
     const double* lw = P.lw + D.dof0;
-    // ---- assemble the lower band (row r: entry d at band[r * bw + d] = A(r, r - d))
-    for (int64_t q = t; q < (int64_t)n * bw; q += kNlThreads) band[q] = 0.0;
+    // ---- lower band of D + Q in global (row r: entry d = A(r, r - d))
+    for (int64_t q = t; q < (int64_t)n * bw; q += NT) band[q] = 0.0;
     __syncthreads();
-    for (int r = t; r < n; r += kNlThreads) band[(size_t)r * bw] = P.ldiag[D.dof0 + r];
-    for (int64_t e = t; e < D.nent; e += kNlThreads) {
-      const int r = P.erow[D.ent0 + e], d = P.eoff[D.ent0 + e];
-      band[(size_t)r * bw + d] = P.eval[D.ent0 + e];
-    }
+    for (int r = t; r < n; r += NT) band[(size_t)r * bw] = P.ldiag[D.dof0 + r];
+    for (int64_t e = t; e < D.nent; e += NT)
+      band[(size_t)P.erow[D.ent0 + e] * bw + P.eoff[D.ent0 + e]] = P.eval[D.ent0 + e];
     __syncthreads();
-    // ---- banded Cholesky, window of rows k..k+b in shared memory (slot = row mod bw)
-    double* W = sm;                       // bw * bw
-    double* lv = sm + bw * bw;            // l_i = L(k+i, k), i = 1..b
-    for (int q = t; q < bw * bw; q += kNlThreads) {
+    // ---- banded Cholesky; ring of R = bw + kWP rows (slot r % R): rows k..k+b live,
+    //      the next kWP rows in flight (cp.async issued kWP columns before they are used)
+    double* W = ws;
+    double* lv = ws + (size_t)R * bw;
+    for (int q = t; q < bw * bw; q += NT) {
       const int r = q / bw;
-      W[q] = r < n ? band[(size_t)r * bw + (q % bw)] : 0.0;
+      W[(size_t)(r % R) * bw + q % bw] = r < n ? band[(size_t)r * bw + q % bw] : 0.0;
     }
-    __syncthreads();
+#pragma unroll 1
+    for (int pq = 0; pq < kWP - 1; ++pq) {               // rows bw .. R-2
+      const int r = bw + pq;
+      if (r < n)
+        for (int q = t; q < bw; q += NT) nl_cp8(W + (size_t)(r % R) * bw + q, band + (size_t)r * bw + q);
+      nl_commit();
+    }
     bool bad = false;
     for (int k = 0; k < n; ++k) {
-      const int sk = k % bw;
-      const double dk = W[sk * bw];
+      const int rn = k + R - 1;                          // into row k-1's slot
+      if (rn < n)
+        for (int q = t; q < bw; q += NT) nl_cp8(W + (size_t)(rn % R) * bw + q, band + (size_t)rn * bw + q);
+      nl_commit();
+      nl_wait<kWP>();                                    // rows up to k+b landed
+      __syncthreads();
+      const int s0 = k % R;
+      const double dk = W[(size_t)s0 * bw];
       if (!(dk > 0.0)) {
         bad = true;
         break;
@@ -104,83 +129,145 @@ __global__ void __launch_bounds__(kNlThreads, 1) nlmc_basis_kernel(const NlParam
       const double s = sqrt(dk);
       const int bk = min(b, n - 1 - k);
       if (t == 0) band[(size_t)k * bw] = s;
-      for (int i = 1 + t; i <= bk; i += kNlThreads) {
-        const double li = W[((k + i) % bw) * bw + i] / s;
+      for (int i = 1 + t; i <= bk; i += NT) {
+        const int si = s0 + i >= R ? s0 + i - R : s0 + i;
+        const double li = W[(size_t)si * bw + i] / s;
         lv[i] = li;
         band[(size_t)(k + i) * bw + i] = li;
       }
       __syncthreads();
-      // trailing update A(k+i, k+j) -= l_i l_j, 1 <= j <= i <= bk: warp per row, lanes over j
-      for (int i = 1 + wid; i <= bk; i += nw) {
-        double* row = W + ((k + i) % bw) * bw;
+      // A(k+i, k+i-d) -= l_i l_{i-d}: warp per row i, lanes over d (contiguous in the row)
+      for (int i = 1 + wid; i <= bk; i += NW) {
+        const int si = s0 + i >= R ? s0 + i - R : s0 + i;
+        double* row = W + (size_t)si * bw;
         const double li = lv[i];
-        for (int j = 1 + lane; j <= i; j += 32) row[i - j] = __fma_rn(-li, lv[j], row[i - j]);
+#pragma unroll 4
+        for (int d = lane; d < i; d += 32) row[d] = __fma_rn(-li, lv[i - d], row[d]);
       }
-      // row k leaves the window, row k + bw enters its slot
-      if (k + bw < n)
-        for (int q = t; q < bw; q += kNlThreads) W[sk * bw + q] = band[(size_t)(k + bw) * bw + q];
-      __syncthreads();
     }
+    nl_wait<0>();
+    __syncthreads();
     if (__syncthreads_or(bad)) {
       if (t == 0) atomicCAS(P.err, 0, di + 1);
       continue;
     }
-    // ---- Z = L^{-T} L^{-1} C^T, all kc columns: thread (c = t % kc, g = t / kc) sums the
-    //      band offsets d = 1 + g, 1 + g + G, ...; fixed-order reduction over g
-    const int G = kNlThreads / kc;
+    // ---- Z = L^{-T} L^{-1} C^T for all kc columns: thread (c, g), G = NT / kc groups
+    //      split the band offsets; one barrier for the partial sums, one for the result
+    double* Lr = ws;                                     // kWP rows (forward) / columns (backward) of L
+    double* Zw = ws + (size_t)kWP * bw;                  // last bw rows of Z, slot r % bw
+    double* part = Zw + (size_t)bw * kc;                 // G * kc partial sums
+    const int G = NT / kc;
     const int c = t % kc, g = t / kc;
     const bool act = g < G;
-    double* lrow = sm;                    // bw values of the current L row / column
-    double* part = sm + 2 * kNlMaxBand;   // G * kc partial sums
-    // forward: y_r = (C^T_r - sum_d L(r, r-d) y_{r-d}) / L(r, r)
+#pragma unroll 1
+    for (int pq = 0; pq < kWP - 1; ++pq) {
+      if (pq < n)
+        for (int q = t; q < bw; q += NT) nl_cp8(Lr + (size_t)pq * bw + q, band + (size_t)pq * bw + q);
+      nl_commit();
+    }
     for (int r = 0; r < n; ++r) {
-      for (int q = t; q < bw; q += kNlThreads) lrow[q] = band[(size_t)r * bw + q];
+      const int rn = r + kWP - 1;
+      if (rn < n)
+        for (int q = t; q < bw; q += NT) nl_cp8(Lr + (size_t)(rn % kWP) * bw + q, band + (size_t)rn * bw + q);
+      nl_commit();
+      nl_wait<kWP - 1>();
       __syncthreads();
-      double acc = 0.0;
-      if (act)
-        for (int d = 1 + g; d <= min(b, r); d += G) acc = __fma_rn(lrow[d], Z[(size_t)(r - d) * kc + c], acc);
-      if (act) part[g * kc + c] = acc;
+      const double* lr = Lr + (size_t)(r % kWP) * bw;
+      const int rs = r % bw;
+      if (act) {
+        double a0 = 0.0, a1 = 0.0;
+        const int dm = min(b, r);
+        int d = 1 + g;
+        int sl = rs - d;                                 // ring slot of row r - d
+        if (sl < 0) sl += bw;
+        for (; d + G <= dm; d += 2 * G) {
+          int s2 = sl - G;
+          if (s2 < 0) s2 += bw;
+          a0 = __fma_rn(lr[d], Zw[sl * kc + c], a0);
+          a1 = __fma_rn(lr[d + G], Zw[s2 * kc + c], a1);
+          sl = s2 - G;
+          if (sl < 0) sl += bw;
+        }
+        if (d <= dm) a0 = __fma_rn(lr[d], Zw[sl * kc + c], a0);
+        part[g * kc + c] = a0 + a1;
+      }
+      const double piv = lr[0];                          // read before the ring slot is reused
       __syncthreads();
       if (t < kc) {
-        double s = 0.0;
-        for (int q = 0; q < G; ++q) s += part[q * kc + t];
+        double sacc = 0.0;
+        for (int q = 0; q < G; ++q) sacc += part[q * kc + t];
         const double rhs = (lcon[r] == t) ? lw[r] : 0.0;
-        Z[(size_t)r * kc + t] = (rhs - s) / lrow[0];
+        const double y = (rhs - sacc) / piv;
+        Zw[rs * kc + t] = y;
+        Z[(size_t)r * kc + t] = y;
       }
-      __syncthreads();
     }
-    // backward: z_r = (y_r - sum_d L(r+d, r) z_{r+d}) / L(r, r)
-    for (int r = n - 1; r >= 0; --r) {
-      for (int q = t; q < bw; q += kNlThreads) lrow[q] = (r + q < n) ? band[(size_t)(r + q) * bw + q] : 0.0;
+    nl_wait<0>();
+    __syncthreads();
+    // backward: z_r = (y_r - sum_d L(r+d, r) z_{r+d}) / L(r, r); column r of L gathered
+#pragma unroll 1
+    for (int pq = 0; pq < kWP - 1; ++pq) {
+      const int r = n - 1 - pq;
+      if (r >= 0)
+        for (int q = t; q < bw; q += NT)
+          if (r + q < n) nl_cp8(Lr + (size_t)(pq % kWP) * bw + q, band + (size_t)(r + q) * bw + q);
+      nl_commit();
+    }
+    for (int tt = 0; tt < n; ++tt) {
+      const int r = n - 1 - tt;
+      const int tn = tt + kWP - 1, rn = n - 1 - tn;
+      if (rn >= 0)
+        for (int q = t; q < bw; q += NT)
+          if (rn + q < n) nl_cp8(Lr + (size_t)(tn % kWP) * bw + q, band + (size_t)(rn + q) * bw + q);
+      nl_commit();
+      nl_wait<kWP - 1>();
       __syncthreads();
-      double acc = 0.0;
-      if (act)
-        for (int d = 1 + g; d <= min(b, n - 1 - r); d += G) acc = __fma_rn(lrow[d], Z[(size_t)(r + d) * kc + c], acc);
-      if (act) part[g * kc + c] = acc;
+      const double* lc = Lr + (size_t)(tt % kWP) * bw;
+      const int rs = r % bw;
+      if (act) {
+        double a0 = 0.0, a1 = 0.0;
+        const int dm = min(b, n - 1 - r);
+        int d = 1 + g;
+        int sl = rs + d;                                 // ring slot of row r + d
+        if (sl >= bw) sl -= bw;
+        for (; d + G <= dm; d += 2 * G) {
+          int s2 = sl + G;
+          if (s2 >= bw) s2 -= bw;
+          a0 = __fma_rn(lc[d], Zw[sl * kc + c], a0);
+          a1 = __fma_rn(lc[d + G], Zw[s2 * kc + c], a1);
+          sl = s2 + G;
+          if (sl >= bw) sl -= bw;
+        }
+        if (d <= dm) a0 = __fma_rn(lc[d], Zw[sl * kc + c], a0);
+        part[g * kc + c] = a0 + a1;
+      }
+      const double piv = lc[0];
       __syncthreads();
       if (t < kc) {
-        double s = 0.0;
-        for (int q = 0; q < G; ++q) s += part[q * kc + t];
-        Z[(size_t)r * kc + t] = (Z[(size_t)r * kc + t] - s) / lrow[0];
+        double sacc = 0.0;
+        for (int q = 0; q < G; ++q) sacc += part[q * kc + t];
+        const double z = (Z[(size_t)r * kc + t] - sacc) / piv;
+        Zw[rs * kc + t] = z;
+        Z[(size_t)r * kc + t] = z;
       }
-      __syncthreads();
     }
-    // ---- S = C Z (kc x kc, shared memory), S(c1, c2) = sum_{l in c1} w_l Z(l, c2)
-    double* S = sm;                       // kc * kc
-    double* y = sm + kNlMaxCons * kNlMaxCons;
-    const int32_t* cp = P.cptr + D.cons0;           // kc + 1 offsets into cidx
-    for (int q = t; q < kc * kc; q += kNlThreads) {
+    nl_wait<0>();
+    __syncthreads();
+    // ---- S = C Z (kc x kc) in shared memory; S(c1, c2) = sum_{l in c1} w_l Z(l, c2)
+    double* S = ws;
+    double* y = ws + (size_t)kc * kc;
+    const int32_t* cp = P.cptr + D.cons0;
+    for (int q = t; q < kc * kc; q += NT) {
       const int c1 = q / kc, c2 = q % kc;
-      double s = 0.0;
+      double acc = 0.0;
       for (int32_t e = cp[c1]; e < cp[c1 + 1]; ++e) {
         const int l = P.cidx[e];
-        s = __fma_rn(lw[l], Z[(size_t)l * kc + c2], s);
+        acc = __fma_rn(lw[l], Z[(size_t)l * kc + c2], acc);
       }
-      S[q] = s;
+      S[q] = acc;
     }
     __syncthreads();
-    // symmetrise (S is symmetric in exact arithmetic) and factor: S = R^T R, dense Cholesky
-    for (int q = t; q < kc * kc; q += kNlThreads) {
+    for (int q = t; q < kc * kc; q += NT) {              // symmetrise (S = S^T exactly)
       const int c1 = q / kc, c2 = q % kc;
       if (c2 > c1) {
         const double v = 0.5 * (S[q] + S[c2 * kc + c1]);
@@ -189,7 +276,7 @@ __global__ void __launch_bounds__(kNlThreads, 1) nlmc_basis_kernel(const NlParam
       }
     }
     __syncthreads();
-    for (int k = 0; k < kc; ++k) {
+    for (int k = 0; k < kc; ++k) {                       // dense Cholesky, lower
       const double dk = S[k * kc + k];
       if (!(dk > 0.0)) {
         bad = true;
@@ -197,12 +284,12 @@ __global__ void __launch_bounds__(kNlThreads, 1) nlmc_basis_kernel(const NlParam
       }
       const double s = sqrt(dk);
       __syncthreads();
-      for (int i = k + 1 + t; i < kc; i += kNlThreads) S[i * kc + k] /= s;
+      for (int i = k + 1 + t; i < kc; i += NT) S[i * kc + k] /= s;
       if (t == 0) S[k * kc + k] = s;
       __syncthreads();
-      for (int q = t; q < (kc - k - 1) * (kc - k - 1); q += kNlThreads) {
-        const int i = k + 1 + q / (kc - k - 1), j = k + 1 + q % (kc - k - 1);
-        if (j <= i) S[i * kc + j] = __fma_rn(-S[i * kc + k], S[j * kc + k], S[i * kc + j]);
+      for (int i = k + 1 + wid; i < kc; i += NW) {
+        const double lik = S[i * kc + k];
+        for (int j = k + 1 + lane; j <= i; j += 32) S[i * kc + j] = __fma_rn(-lik, S[j * kc + k], S[i * kc + j]);
       }
       __syncthreads();
     }
@@ -210,27 +297,27 @@ __global__ void __launch_bounds__(kNlThreads, 1) nlmc_basis_kernel(const NlParam
       if (t == 0) atomicCAS(P.err, 0, di + 1);
       continue;
     }
-    // ---- psi = Z S^{-1} e_own for every own coarse DOF
+    // ---- psi = Z S^{-1} e_own for every coarse DOF of cell i
     for (int o = 0; o < D.nown; ++o) {
       const int ce = P.own_con[D.own0 + o];
-      if (t == 0) {                                   // kc <= 128: serial triangular solves
+      if (t == 0) {                                      // kc <= 128: serial triangular solves
         for (int i = 0; i < kc; ++i) {
-          double s = (i == ce) ? 1.0 : 0.0;
-          for (int j = 0; j < i; ++j) s = __fma_rn(-S[i * kc + j], y[j], s);
-          y[i] = s / S[i * kc + i];
+          double sacc = (i == ce) ? 1.0 : 0.0;
+          for (int j = 0; j < i; ++j) sacc = __fma_rn(-S[i * kc + j], y[j], sacc);
+          y[i] = sacc / S[i * kc + i];
         }
         for (int i = kc - 1; i >= 0; --i) {
-          double s = y[i];
-          for (int j = i + 1; j < kc; ++j) s = __fma_rn(-S[j * kc + i], y[j], s);
-          y[i] = s / S[i * kc + i];
+          double sacc = y[i];
+          for (int j = i + 1; j < kc; ++j) sacc = __fma_rn(-S[j * kc + i], y[j], sacc);
+          y[i] = sacc / S[i * kc + i];
         }
       }
       __syncthreads();
       double* out = P.psi + P.own_psi[D.own0 + o];
-      for (int l = t; l < n; l += kNlThreads) {
-        double s = 0.0;
-        for (int q = 0; q < kc; ++q) s = __fma_rn(Z[(size_t)l * kc + q], y[q], s);
-        out[l] = s;
+      for (int l = t; l < n; l += NT) {
+        double acc = 0.0;
+        for (int q = 0; q < kc; ++q) acc = __fma_rn(Z[(size_t)l * kc + q], y[q], acc);
+        out[l] = acc;
       }
       __syncthreads();
     }
@@ -512,6 +599,7 @@ extern "C" mc_status mc_nlmc_build(mc_ctx* fine, const mc_nlmc_desc* d, mc_nlmc*
   int64_t psi_len = 0;
   std::vector<int32_t> loc((size_t)N, -1);
   int nmax = 1, bmax = 0, kcmax = 1;
+  int64_t spw_need = 1;
   for (int i = 0; i < nHx * nHy; ++i) {
     if (owned[(size_t)i].empty()) continue;
     const int iy = i / nHx, ix = i % nHx;
@@ -585,7 +673,12 @@ extern "C" mc_status mc_nlmc_build(mc_ctx* fine, const mc_nlmc_desc* d, mc_nlmc*
     nmax = std::max(nmax, D.n);
     bmax = std::max(bmax, b);
     kcmax = std::max(kcmax, D.kc);
-    if (b > kNlMaxBand - 1 || D.kc > kNlMaxCons || (b + 1) * (b + 1) + kNlMaxBand > kNlSmemDoubles) {
+    const int64_t need = std::max<int64_t>((int64_t)(b + 1 + kWP) * (b + 1) + b + 1,
+                                           std::max<int64_t>((int64_t)kWP * (b + 1) + (int64_t)(b + 1) * D.kc +
+                                                                 (int64_t)(kNlThreads / std::max(1, D.kc)) * D.kc,
+                                                             (int64_t)D.kc * D.kc + D.kc));
+    spw_need = std::max<int64_t>(spw_need, need);
+    if (D.kc > kNlMaxCons || need > kNlSmemDoubles) {
       snprintf(msg, sizeof msg, "NLMC: region of coarse cell %d too large for one CTA (bandwidth %d, %d constraints)",
                i, b, D.kc);
       delete nl;
@@ -597,7 +690,11 @@ extern "C" mc_status mc_nlmc_build(mc_ctx* fine, const mc_nlmc_desc* d, mc_nlmc*
   int dev = 0, sms = 0;
   NL_CUDA(cudaGetDevice(&dev));
   NL_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-  const int grid = std::max(1, std::min<int>((int)dom.size(), sms));
+  // one region per CTA; as many CTAs per SM as their shared memory allows (<= 8)
+  const int spw = (int)((spw_need + 1) & ~int64_t(1));
+  const int wpb = 1;
+  const int per_sm = std::max(1, std::min<int>(8, (228 * 1024) / (spw * 8 + 2048)));
+  const int grid = std::max(1, std::min<int>((int)dom.size(), sms * per_sm));
   DevBufs B;
   NlParams P{};
   NlDomain* ddom;
@@ -618,8 +715,8 @@ extern "C" mc_status mc_nlmc_build(mc_ctx* fine, const mc_nlmc_desc* d, mc_nlmc*
   NL_CUDA(B.put(&down_psi, own_psi));
   P.band_stride = (int64_t)nmax * (bmax + 1);
   P.z_stride = (int64_t)nmax * kcmax;
-  NL_CUDA(B.alloc(&dband, (size_t)grid * P.band_stride));
-  NL_CUDA(B.alloc(&dZ, (size_t)grid * P.z_stride));
+  NL_CUDA(B.alloc(&dband, (size_t)grid * wpb * P.band_stride));
+  NL_CUDA(B.alloc(&dZ, (size_t)grid * wpb * P.z_stride));
   NL_CUDA(B.alloc(&dpsi, (size_t)psi_len));
   NL_CUDA(B.alloc(&derr, 1));
   NL_CUDA(cudaMemset(derr, 0, sizeof(int32_t)));
@@ -640,7 +737,9 @@ extern "C" mc_status mc_nlmc_build(mc_ctx* fine, const mc_nlmc_desc* d, mc_nlmc*
   P.Z = dZ;
   P.psi = dpsi;
   P.err = derr;
-  const size_t smem = (size_t)kNlSmemDoubles * sizeof(double);
+  P.wpb = wpb;
+  P.spw = spw;
+  const size_t smem = (size_t)wpb * spw * sizeof(double);
   NL_CUDA(cudaFuncSetAttribute(nlmc_basis_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   cudaEvent_t e0, e1, e2;
   NL_CUDA(cudaEventCreate(&e0));
@@ -712,7 +811,9 @@ extern "C" mc_status mc_nlmc_build(mc_ctx* fine, const mc_nlmc_desc* d, mc_nlmc*
   Q.cell = dcell;
   Q.nHx = nHx;
   Q.out = dout;
-  NL_CUDA(cudaEventRecord(e1));
+  cudaEvent_t e3;
+  NL_CUDA(cudaEventCreate(&e3));
+  NL_CUDA(cudaEventRecord(e3));
   nlmc_project_kernel<<<std::max(1, std::min<int>((int)((pr.size() + 7) / 8), 8 * sms)), 256>>>(Q);
   NL_CUDA(cudaGetLastError());
   NL_CUDA(cudaEventRecord(e2));
@@ -720,7 +821,8 @@ extern "C" mc_status mc_nlmc_build(mc_ctx* fine, const mc_nlmc_desc* d, mc_nlmc*
   NL_CUDA(cudaMemcpy(dv.data(), dout, dv.size() * sizeof(double), cudaMemcpyDeviceToHost));
   float t1 = 0.f, t2 = 0.f;
   NL_CUDA(cudaEventElapsedTime(&t1, e0, e1));
-  NL_CUDA(cudaEventElapsedTime(&t2, e1, e2));
+  NL_CUDA(cudaEventElapsedTime(&t2, e3, e2));
+  cudaEventDestroy(e3);
   cudaEventDestroy(e0);
   cudaEventDestroy(e1);
   cudaEventDestroy(e2);
