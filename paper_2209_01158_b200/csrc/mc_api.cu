@@ -22,6 +22,7 @@ using namespace mc;
 namespace {
 
 constexpr int64_t kLargeRows = int64_t(2) << 20;   // "bandwidth-bound" solve
+constexpr int64_t kOneCtaWork = 0;                   // rows + stored entries below which a solve gets one CTA
 
 struct HostCont {
   bool set = false;
@@ -881,7 +882,19 @@ static int64_t default_maxit(const mc_ctx* c, int64_t n) {
 }
 
 // CTAs a latency-bound solve of n rows can use with >= 2 rows per thread
+// A solve whose pass is this small runs on ONE CTA: its reduction is a CTA barrier
+// (~0.1 us) instead of a grid-wide one (>= 1.8 us, profiles/r01_barrier.txt).
+static int64_t one_cta_work() {
+  static const int64_t w = [] {
+    const char* e = getenv("MC_ONE_CTA_WORK");
+    return e ? (int64_t)atoll(e) : (int64_t)kOneCtaWork;
+  }();
+  return w;
+}
+
 static int useful_ctas(const HostCont& H) {
+  const int64_t work = H.kind == KIND_GRID ? 5 * H.n : H.n + H.col_count;
+  if (work <= one_cta_work()) return 1;
   const int64_t lanes = (H.kind == KIND_GRAPH && H.col_count > 8 * H.n) ? 8 * H.n : H.n;
   return (int)std::max<int64_t>(1, (lanes + 2 * kThreads - 1) / (2 * kThreads));
 }

@@ -1046,16 +1046,34 @@ template <int NP>
 __device__ __forceinline__ void group_allreduce(const StepParams& P, int g, int cl,
                                                 unsigned long long& epoch, const double (&v)[NP],
                                                 double (&out)[NP]) {
-  __shared__ double sh[kWarps][kNPart];
+  __shared__ double sh[2][kWarps][kNPart];
   __shared__ double tot[kNPart];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int G = P.grp[g].cta_count, base = P.grp[g].cta_begin;
+  const int eb = (int)(epoch & 1ull);
 #pragma unroll
   for (int k = 0; k < NP; ++k) {
     double s = v[k];
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-    if (lane == 0) sh[w][k] = s;
+    if (lane == 0) sh[eb][w][k] = s;
+  }
+  if (G == 1) {
+    // one-CTA group: the CTA barrier orders this pass's global writes before the next
+    // pass's reads (bar.sync), the proxy fence makes them visible to the TMA copies;
+    // every thread sums the warp partials in the same fixed order, so the result is
+    // bitwise the multi-CTA path's at G = 1.  sh is parity-buffered: one barrier.
+    asm volatile("fence.proxy.async.global;" ::: "memory");
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < NP; ++k) {
+      double s = 0.0;
+#pragma unroll
+      for (int i = 0; i < kWarps; ++i) s += sh[eb][i][k];
+      out[k] = s + 0.0;
+    }
+    ++epoch;
+    return;
   }
   __syncthreads();
   double* part = P.partials + (size_t)(epoch & 1ull) * kNPart * P.total_ctas;
@@ -1065,7 +1083,7 @@ __device__ __forceinline__ void group_allreduce(const StepParams& P, int g, int 
     for (int k = 0; k < NP; ++k) {
       double s = 0.0;
 #pragma unroll
-      for (int i = 0; i < kWarps; ++i) s += sh[i][k];
+      for (int i = 0; i < kWarps; ++i) s += sh[eb][i][k];
       __stcg(part + (size_t)k * P.total_ctas + base + cl, s);
     }
     // release: this CTA's r/p/q stores (ordered before by bar.sync) and its partials
