@@ -48,6 +48,9 @@ def parse():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--precond", default="jacobi", choices=["jacobi", "block"],
+                    help="CG preconditioner: jacobi (the north star's, default) or block "
+                         "(block-Jacobi on the fracture network, mc_set_preconditioner)")
     return ap.parse_args()
 
 
@@ -267,7 +270,7 @@ def main():
     scn = make(args.config)
     stream = torch.cuda.Stream()
     torch.cuda.set_stream(stream)
-    pb = Problem(scn, device=local, stream=stream, rtols=CONFIG_RTOL[args.config])
+    pb = Problem(scn, device=local, stream=stream, rtols=CONFIG_RTOL[args.config], precond=args.precond)
     pb.byte_model = model_for(scn)
     dof = sum(pb.sizes)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
@@ -295,7 +298,8 @@ def main():
     kern_ms = sum(r["ms"] for r in reps) / args.steps
     peak, peak_src = peaks()
     achieved = bytes_per / (kern_ms * 1e-3) / 1e9
-    traffic, traffic_src = ncu_traffic(args.config, 3) if args.scheme == "D" else (None, None)
+    traffic, traffic_src = (ncu_traffic(args.config, 3) if args.scheme == "D" and args.precond == "jacobi"
+                            else (None, None))
     # end to end through the C ABI with host buffers (pinned), copies inside the timed region
     e2e = None
     if not args.no_e2e:
@@ -335,6 +339,7 @@ def main():
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": workload_name(args.config, args.scheme), "dof": dof,
                        "sizes": pb.sizes, "scheme": args.scheme, "rtol": CONFIG_RTOL[args.config] or 1e-12,
+                       "precond": args.precond,
                        "cg_iters_per_step": mean_its,
                        "ms_per_solve": [sum(r["ms_solve"][a] for r in reps) / len(reps) for a in range(len(reps[0]["ms_solve"]))],
                        "l2": "flushed between timed steps (256 MiB memset)",

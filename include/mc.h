@@ -182,6 +182,16 @@ mc_status mc_set_continuum(mc_ctx* ctx, int32_t alpha, const mc_continuum_desc* 
 /* Add a transfer Q_ab.  All continua must be set first (else MC_ERR_STATE). */
 mc_status mc_set_coupling(mc_ctx* ctx, const mc_coupling_desc* desc);
 
+/* CG preconditioner (the paper defers solver comparison,
+ * PAPER.md:852).  MC_PRECOND_JACOBI (default): D^{-1} = 1/diag(K) (reading C14).
+ * MC_PRECOND_BLOCK: for graph continua with <= 4 connections per cell and uniform T
+ * (fracture networks): the cells are renumbered in chain order and M = the tridiagonal
+ * part of K on every 64-cell block (cells i, i+1 of a block connected along the network),
+ * solved exactly; other continua keep Jacobi.  Same solution, fewer iterations; two
+ * reductions per iteration instead of one.  Must precede mc_set_continuum. */
+typedef enum { MC_PRECOND_JACOBI = 0, MC_PRECOND_BLOCK = 1 } mc_precond;
+mc_status mc_set_preconditioner(mc_ctx* ctx, int32_t kind);
+
 /* Order of the continua by ascending permeability k_1 < k_2 < ...:
  * order[0] is the least permeable.  Required before MC_DECOUPLED_L / MC_DECOUPLED_U. */
 mc_status mc_set_permeability_order(mc_ctx* ctx, const int32_t* order);

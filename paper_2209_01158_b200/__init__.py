@@ -6,6 +6,6 @@ ctypes binding.  Importing this package does not load the library; ``mc.load()``
 (or constructing ``mc.Problem``) does, and raises if it has not been built.
 """
 from . import mc  # noqa: F401
-from .mc import Problem, load, MCError  # noqa: F401
+from .mc import Problem, load, MCError, permeability_order  # noqa: F401
 
 __all__ = ["mc", "Problem", "load", "MCError"]

@@ -39,6 +39,7 @@ struct HostCont {
   double rtol = 0.0;                           // per-continuum CG tolerance (D-scheme)
   int64_t col_count = 0;                       // graph: stored off-diagonal entries
   int64_t estride = 0;                         // graph: ELL stride
+  bool bj = false;                             // graph: block-Jacobi preconditioner (mc_set_preconditioner)
   std::vector<int32_t> perm, inv;              // graph: internal position -> caller index, inverse
   std::vector<uint8_t> fixed;                  // graph Dirichlet DOFs
   std::vector<double> gfix;
@@ -85,6 +86,10 @@ struct mc_ctx {
   double* val[MC_MAX_CONTINUA] = {nullptr};
   int32_t* ecol[MC_MAX_CONTINUA] = {nullptr};
   int32_t* perm[MC_MAX_CONTINUA] = {nullptr};   // graph: internal -> caller numbering
+  double* tinv[MC_MAX_CONTINUA] = {nullptr};    // bj: chunk Thomas factors
+  double* tcp[MC_MAX_CONTINUA] = {nullptr};
+  double* tem[MC_MAX_CONTINUA] = {nullptr};
+  int32_t precond = 0;                           // MC_PRECOND_*
   double* scratch = nullptr;                     // state I/O staging (max graph n)
   double* partials = nullptr;
   SyncBlock* sync = nullptr;
@@ -607,7 +612,8 @@ extern "C" mc_status mc_set_continuum(mc_ctx* c, int32_t alpha, const mc_continu
     int maxdeg = 0;
     for (int64_t i = 0; i < H.n; ++i) maxdeg = std::max(maxdeg, H.rowptr[(size_t)i + 1] - H.rowptr[(size_t)i]);
     const char* ch = getenv("MC_CHAIN");
-    if (maxdeg <= 4 && ch && ch[0] == '1') apply_chain_order(H);
+    H.bj = (c->precond == MC_PRECOND_BLOCK) && maxdeg <= 4 && H.val.empty();
+    if (maxdeg <= 4 && ((ch && ch[0] == '1') || H.bj)) apply_chain_order(H);
   }
   H.set = true;
   c->hc[alpha] = std::move(H);
@@ -782,6 +788,35 @@ static mc_status finalize(mc_ctx* c) {
           }
         }
         UP(c->ecol[a], ell);
+        if (H.bj) {
+          // block-Jacobi: tridiagonal part of every 64-row chunk (rows i, i+1 of the
+          // chunk connected along the chain-ordered network), factored once (Thomas)
+          std::vector<double> inv(NS, 1.0), cpv(NS, 0.0), em(NS, 0.0);
+          auto linked = [&](int64_t i) {            // i -- i+1 connected
+            for (int32_t e = H.rowptr[(size_t)i]; e < H.rowptr[(size_t)i + 1]; ++e)
+              if (H.col[(size_t)e] == i + 1) return true;
+            return false;
+          };
+          for (int64_t i0 = 0; i0 < H.n; i0 += 64) {
+            const int64_t i1 = std::min<int64_t>(H.n, i0 + 64);
+            double cprev = 0.0, eprev = 0.0;
+            for (int64_t i = i0; i < i1; ++i) {
+              const size_t gi = (size_t)(c->off[a] + i);
+              const double ai = dsD[gi] + tsum[gi];
+              const double den = ai - eprev * cprev;
+              if (!(den > 0.0)) return fail(c, MC_ERR_ARG, "continuum %d: block-Jacobi pivot %g not > 0", a, den);
+              const double ei = (i + 1 < i1 && linked(i)) ? -H.Tconst : 0.0;
+              inv[gi] = 1.0 / den;
+              em[gi] = eprev;
+              cprev = ei / den;
+              cpv[gi] = cprev;
+              eprev = ei;
+            }
+          }
+          UP(c->tinv[a], inv);
+          UP(c->tcp[a], cpv);
+          UP(c->tem[a], em);
+        }
       }
       if (!H.perm.empty()) UP(c->perm[a], H.perm);
       UP(c->rowptr[a], H.rowptr);
@@ -1084,7 +1119,14 @@ static mc_status enqueue_step(mc_ctx* c, int scheme) {
       if (((G.cont_mask >> a) & 1) && P.cont[a].rr) {
         const int64_t nch = (c->hc[a].n + 63) / 64;
         P.cont[a].resident = (nconts == 1 && nch <= (int64_t)kStages * G.cta_count * kWarps) ? 1 : 0;
+        P.cont[a].bj = (nconts == 1 && nch <= (int64_t)G.cta_count * kWarps && c->tinv[a] != nullptr &&
+                        scheme != MC_COUPLED) ? 1 : 0;
       }
+  }
+  for (int a = 0; a < c->L; ++a) {
+    P.cont[a].tinv = c->tinv[a];
+    P.cont[a].tcp = c->tcp[a];
+    P.cont[a].tem = c->tem[a];
   }
   P.L = c->L;
   P.ngroups = cp.ngroups;
@@ -1171,6 +1213,15 @@ extern "C" mc_status mc_step_coupled(mc_ctx* c, mc_step_report* rep) {
 }
 
 extern "C" mc_status mc_step(mc_ctx* c, int32_t scheme, mc_step_report* rep) { return do_step(c, scheme, rep); }
+
+extern "C" mc_status mc_set_preconditioner(mc_ctx* c, int32_t kind) {
+  if (!c) return fail(c, MC_ERR_ARG, "NULL context");
+  if (kind != MC_PRECOND_JACOBI && kind != MC_PRECOND_BLOCK) return fail(c, MC_ERR_ARG, "preconditioner %d unknown", kind);
+  for (int a = 0; a < c->L; ++a)
+    if (c->hc[a].set) return fail(c, MC_ERR_STATE, "mc_set_preconditioner after mc_set_continuum");
+  c->precond = kind;
+  return MC_OK;
+}
 
 extern "C" mc_status mc_set_permeability_order(mc_ctx* c, const int32_t* order) {
   if (!c || !order) return fail(c, MC_ERR_ARG, "NULL argument");

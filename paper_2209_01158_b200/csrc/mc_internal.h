@@ -57,6 +57,10 @@ struct ContDev {
   int64_t estride;         // graph: ELL row stride (n rounded up to 64, + 64)
   int32_t rr;              // 1: processed by the whole group, 64-row chunks round-robin over warps
   int32_t resident;        // rr + every warp owns <= kStages chunks: state stays in shared memory
+  int32_t bj;              // resident, one chunk per warp, block-Jacobi preconditioner (§8(f) rank 4)
+  const double* tinv;      // bj: Thomas factors of each 64-row chunk's tridiagonal block:
+  const double* tcp;       //     1 / pivot, super-diagonal multiplier c', sub-diagonal e_{i-1}
+  const double* tem;
 };
 
 // a work item: a 32-column strip segment of a grid, or a row range of a graph

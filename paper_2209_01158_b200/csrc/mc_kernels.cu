@@ -306,6 +306,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
       : "memory");
 }
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+__device__ __forceinline__ void fence_proxy_async_shared_global() { asm volatile("fence.proxy.async.global;" ::: "memory"); }
 
 // per-warp staging state: slots of doubles, one mbarrier per slot, slot parities
 struct Stage {
@@ -1124,6 +1125,250 @@ __device__ __forceinline__ void group_allreduce(const StepParams& P, int g, int 
   ++epoch;
 }
 
+
+// ---------------------------------------------------------------- block-Jacobi PCG (bj)
+// Optional preconditioner (mc_set_preconditioner): M = the
+// tridiagonal part of each 64-row chunk of a chain-ordered graph continuum (consecutive
+// rows of a chunk connected along the network), solved exactly in shared memory with the
+// chunk's precomputed Thomas factors.  Standard PCG, two reductions per iteration:
+//   pass S:  p_j = z_j + beta p_{j-1} (own rows; far neighbours recomputed from their
+//            published z, p_{j-1}), q = K p_j, partial p.q            -> alpha
+//   pass U:  x += alpha p_j, r -= alpha q, z = M^{-1} r, partials r.z, r.r -> beta, stop
+// The iterates solve the same SPD system; only the iteration count changes.
+__device__ __forceinline__ void bj_solve(const double* sl, double* zc, int lane) {
+  // z = M^{-1} r over the chunk: lane 0 sweeps (64 steps each way), rows in the slot
+  if (lane == 0) {
+    const double* r = sl + 2;
+    const double* inv = sl + 206;
+    const double* cp = zc + 64;
+    const double* em = zc + 128;
+    double dprev = 0.0;
+    for (int i = 0; i < 64; ++i) {
+      dprev = (r[i] - em[i] * dprev) * inv[i];
+      zc[i] = dprev;
+    }
+    double zn = zc[63];
+    for (int i = 62; i >= 0; --i) {
+      zn = __fma_rn(-cp[i], zn, zc[i]);
+      zc[i] = zn;
+    }
+  }
+  __syncwarp();
+}
+
+__device__ void run_group_bj(const StepParams& P, int g, int cl, double* x, const double* uo) {
+  const Group& G = P.grp[g];
+  const int W = G.cta_count * kWarps;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int wg = cl * kWarps + wid;
+  const bool leader = (cl == 0 && threadIdx.x == 0);
+  const long long t0 = leader ? globaltimer() : 0;
+  const ContDev& C = P.cont[__ffs(G.cont_mask) - 1];
+  extern __shared__ __align__(16) double dsm[];
+  Stage st;
+  st.wsm = dsm + wid * kWarpSmem;
+  st.bars = reinterpret_cast<uint64_t*>(dsm + kWarps * kWarpSmem) + wid * kNBars;
+  st.ph = reinterpret_cast<unsigned*>(dsm + kWarps * kWarpSmem + kWarps * kNBars) + 2 * wid;
+  double* sl = st.wsm;                 // slot 0: r, q, p, 1/pivot, x, shift, codes
+  double* zc = st.wsm + kSlotE;        // slot 1: z, c', e_{i-1}
+  const int64_t off = C.off, es = C.estride;
+  const int r1 = (int)C.n, nch = (r1 + 63) / 64;
+  const int m = wg;                    // this warp's chunk (one per warp)
+  const bool own = m < nch;
+  const int base = 64 * m + 2 * lane;
+  const int64_t g0 = off + base;
+  const bool ok0 = own && base < r1, ok1 = own && base + 1 < r1;
+  double* zg = P.q[0];                 // published z (global), read by far neighbours
+  // init (a1, a2): lagged right-hand side, r0 = b - K x0, x0 = u^{n-1}
+  double a3[3] = {0.0, 0.0, 0.0};
+  for (int mm = wg; 32 * mm < r1; mm += W) {
+    Item rit{};
+    rit.cont = __ffs(G.cont_mask) - 1;
+    rit.kind = ITEM_GRAPH;
+    rit.a = 32 * mm;
+    rit.b = min(32 * mm + 32, r1);
+    init_item<false>(P, rit, uo, x, G.phase, a3);
+  }
+  unsigned long long epoch = 0;
+  double t3[3];
+  group_allreduce<3>(P, g, cl, epoch, a3, t3);
+  const double bb = t3[0];
+  double rr = t3[1];
+  int64_t iters = 0;
+  int status = MC_OK;
+  bool zero = false, ran = false;
+  if (bb == 0.0) {
+    zero = true;
+    rr = 0.0;
+  } else if (!(rr <= G.tol2 * bb)) {
+    ran = true;
+    // own chunk -> shared memory: r, p (= 0), 1/pivot, x, shift, codes; z factors
+    fence_proxy_async_shared_global();
+    if (own) {
+      __syncwarp();
+      if (lane == 0) {
+        const int64_t b0 = 64 * (int64_t)m, gg = off + b0;
+        st.begin(0, 4u * 512u + 4u * 256u);
+        uint64_t* bar = st.bars;
+        bulk_g2s(sl + 2, P.r[0] + gg, 512, bar);
+        bulk_g2s(sl + 206, C.tinv + gg, 512, bar);
+        bulk_g2s(sl + 272, x + gg, 512, bar);
+        bulk_g2s(sl + 336, P.dsD + gg, 512, bar);
+        int32_t* si = reinterpret_cast<int32_t*>(sl + 400);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) bulk_g2s(si + k * 64, C.ecol + k * es + b0, 256, bar);
+        st.begin(1, 2u * 512u);
+        bulk_g2s(zc + 64, C.tcp + gg, 512, st.bars + 1);
+        bulk_g2s(zc + 128, C.tem + gg, 512, st.bars + 1);
+      }
+      st.wait(0);
+      st.wait(1);
+      // decode ELL codes into global columns (-1 none); p_{-1} = 0
+      int32_t* si = reinterpret_cast<int32_t*>(sl + 400);
+      const int64_t cb = off + 64 * (int64_t)m;
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int e = lane + 32 * u, cd = si[e];
+        si[e] = cd <= -2 ? (int32_t)(cb + (-2 - cd) - 2) : cd;
+      }
+      sl[138 + 2 * lane] = 0.0;
+      sl[139 + 2 * lane] = 0.0;
+      __syncwarp();
+    }
+    // U_0: z_0 = M^{-1} r_0, publish, r.z
+    double rz = 0.0;
+    {
+      double a2[2] = {0.0, 0.0};
+      if (own) {
+        bj_solve(sl, zc, lane);
+#pragma unroll
+        for (int h = 0; h < 2; ++h)
+          if (base + h < r1) {
+            const double rv = sl[2 + 2 * lane + h], zv = zc[2 * lane + h];
+            stmut(zg + g0 + h, zv);
+            stmut(P.p[1] + g0 + h, 0.0);
+            a2[0] += rv * zv;
+            a2[1] += rv * rv;
+          }
+      }
+      double t2[2];
+      group_allreduce<2>(P, g, cl, epoch, a2, t2);
+      rz = t2[0];
+    }
+    double beta = 0.0;
+    const int32_t* si = reinterpret_cast<const int32_t*>(sl + 400);
+    for (int64_t j = 0;; ++j) {
+      // ---- pass S: p_j = z_j + beta p_{j-1}; q = K p_j; p.q
+      const double* pold = P.p[(j + 1) & 1];
+      double* pnew_g = P.p[j & 1];
+      double a1[1] = {0.0};
+      if (own) {
+        double pc[2];
+        int32_t jc[2][4];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int l2 = 2 * lane + h;
+          pc[h] = __fma_rn(beta, sl[138 + l2], zc[l2]);
+#pragma unroll
+          for (int k = 0; k < 4; ++k) jc[h][k] = si[k * 64 + l2];
+        }
+        // far neighbours: recompute p from their published z and p_{j-1}
+        double pf[2][4];
+        const int64_t cb = off + 64 * (int64_t)m;
+#pragma unroll
+        for (int h = 0; h < 2; ++h)
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            const int64_t jj = jc[h][k];
+            const int64_t li = jj - cb;
+            pf[h][k] = 0.0;
+            if (jj >= 0 && !(li >= 0 && li < 64)) pf[h][k] = __fma_rn(beta, ldnb(pold + jj), ldnb(zg + jj));
+          }
+        __syncwarp();
+        sl[138 + 2 * lane] = pc[0];
+        sl[139 + 2 * lane] = pc[1];
+        if (ok1) st2mut(pnew_g + g0, make_double2(pc[0], pc[1]));
+        else if (ok0) stmut(pnew_g + g0, pc[0]);
+        __syncwarp();
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          double s = 0.0;
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            const int64_t jj = jc[h][k];
+            const int64_t li = jj - cb;
+            const bool in = jj >= 0 && li >= 0 && li < 64;
+            const double v = jj < 0 ? pc[h] : (in ? sl[138 + (int)li] : pf[h][k]);
+            s += pc[h] - v;
+          }
+          const double qv = sl[336 + 2 * lane + h] * pc[h] + C.Tconst * s;
+          sl[70 + 2 * lane + h] = qv;
+          if (base + h < r1) a1[0] += pc[h] * qv;
+        }
+      }
+      double t1[1];
+      group_allreduce<1>(P, g, cl, epoch, a1, t1);
+      if (!(t1[0] > 0.0)) {
+        iters = j;
+        status = MC_ERR_BREAKDOWN;
+        break;
+      }
+      const double alpha = rz / t1[0];
+      // ---- pass U: x += alpha p; r -= alpha q; z = M^{-1} r; r.z, r.r
+      double a2[2] = {0.0, 0.0};
+      if (own) {
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int l2 = 2 * lane + h;
+          sl[272 + l2] = __fma_rn(alpha, sl[138 + l2], sl[272 + l2]);
+          sl[2 + l2] = __fma_rn(-alpha, sl[70 + l2], sl[2 + l2]);
+        }
+        __syncwarp();
+        bj_solve(sl, zc, lane);
+#pragma unroll
+        for (int h = 0; h < 2; ++h)
+          if (base + h < r1) {
+            const double rv = sl[2 + 2 * lane + h], zv = zc[2 * lane + h];
+            stmut(zg + g0 + h, zv);
+            a2[0] += rv * zv;
+            a2[1] += rv * rv;
+          }
+      }
+      double t2[2];
+      group_allreduce<2>(P, g, cl, epoch, a2, t2);
+      rr = t2[1];
+      iters = j + 1;
+      if (rr <= G.tol2 * bb) break;
+      if (j + 1 >= G.maxit) {
+        status = MC_ERR_NOCONV;
+        break;
+      }
+      if (!(t2[0] > 0.0)) {
+        status = MC_ERR_BREAKDOWN;
+        break;
+      }
+      beta = t2[0] / rz;
+      rz = t2[0];
+    }
+  }
+  if (ran && own)
+    for (int h = 0; h < 2; ++h)
+      if (base + h < r1) x[g0 + h] = sl[272 + 2 * lane + h];
+  if (zero)
+    for (int64_t i = (int64_t)wg * 32 + lane; i < C.n; i += (int64_t)W * 32) x[C.off + i] = 0.0;
+  if (leader) {
+    GroupOut o;
+    o.iters = iters;
+    o.status = status;
+    o.pad = 0;
+    o.bb = bb;
+    o.rr = rr;
+    o.t0 = t0;
+    o.t1 = globaltimer();
+    P.gout[g] = o;
+  }
+}
+
 // ---------------------------------------------------------------- the step kernel
 template <bool CPL>
 __device__ void run_group(const StepParams& P, int g, int cl, double* x, const double* uo) {
@@ -1289,7 +1534,9 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) step_kernel(const __grid
         if (G.phase != ph || (int)blockIdx.x < G.cta_begin || (int)blockIdx.x >= G.cta_begin + G.cta_count)
           continue;
         const int cl = (int)blockIdx.x - G.cta_begin;
+        const int a0 = __ffs(G.cont_mask) - 1;
         if (P.coupled) run_group<true>(P, g, cl, x, uo);
+        else if ((G.cont_mask & (G.cont_mask - 1)) == 0 && P.cont[a0].bj) run_group_bj(P, g, cl, x, uo);
         else run_group<false>(P, g, cl, x, uo);
       }
       if (ph + 1 < P.nphases) grid_barrier(P, (unsigned long long)(ph + 1) * gridDim.x);

@@ -69,7 +69,7 @@ class mc_step_report(C.Structure):
 
 
 EXPORTS = ["mc_create", "mc_set_continuum", "mc_set_coupling", "mc_step_decoupled", "mc_step_coupled",
-           "mc_step", "mc_set_permeability_order",
+           "mc_step", "mc_set_permeability_order", "mc_set_preconditioner",
            "mc_run", "mc_get_state", "mc_set_state", "mc_size", "mc_last_kernel_ms", "mc_destroy",
            "mc_error_string", "mc_abi_version", "mc_nlmc_build", "mc_nlmc_sizes", "mc_nlmc_get",
            "mc_nlmc_basis", "mc_nlmc_times", "mc_nlmc_error_string", "mc_nlmc_destroy"]
@@ -95,6 +95,7 @@ def load(path: str | None = None):
     lib.mc_step_coupled.argtypes = [P, C.POINTER(mc_step_report)]
     lib.mc_step.argtypes = [P, _i32, C.POINTER(mc_step_report)]
     lib.mc_set_permeability_order.argtypes = [P, C.c_void_p]
+    lib.mc_set_preconditioner.argtypes = [P, _i32]
     lib.mc_run.argtypes = [P, _i32, _i32, C.POINTER(mc_step_report), C.POINTER(C.c_void_p)]
     lib.mc_get_state.argtypes = [P, _i32, C.c_void_p]
     lib.mc_set_state.argtypes = [P, _i32, C.c_void_p]
@@ -163,8 +164,9 @@ class Problem:
     """
 
     def __init__(self, scn, tau=None, rtol=1e-12, maxit=0, ctas=0, device=0, stream=None,
-                 host_inputs=False, rtols=None):
-        """rtols: optional per-continuum CG tolerances (D-scheme), default rtol for all."""
+                 host_inputs=False, rtols=None, precond="jacobi"):
+        """rtols: optional per-continuum CG tolerances (D-scheme), default rtol for all.
+        precond: "jacobi" (default, the north star's) or "block" (mc_set_preconditioner)."""
         import torch
         self.lib = load()
         self.torch = torch
@@ -185,6 +187,7 @@ class Problem:
             for d, t in zip(conts, rtols):
                 d.rtol = float(t)
         self._check(self.lib.mc_create(C.byref(self.ctx), self.L, C.byref(opt)), create=True)
+        self._check(self.lib.mc_set_preconditioner(self.ctx, {"jacobi": 0, "block": 1}[precond]))
         for a, d in enumerate(conts):
             self._check(self.lib.mc_set_continuum(self.ctx, a, C.byref(d)))
         for d in cpls:
