@@ -118,11 +118,12 @@ __global__ void __launch_bounds__(kNlThreads) nlmc_basis_kernel(const NlParams P
       if (rn < n)
         for (int q = t; q < bw; q += NT) nl_cp8(W + (size_t)(rn % R) * bw + q, band + (size_t)rn * bw + q);
       nl_commit();
+      const double akk = __ldg(P.ldiag + D.dof0 + k);   // unfactored diagonal
       nl_wait<kWP>();                                    // rows up to k+b landed
       __syncthreads();
       const int s0 = k % R;
       const double dk = W[(size_t)s0 * bw];
-      if (!(dk > 0.0)) {
+      if (!(dk > 1e-13 * akk)) {                         // (numerically) singular region
         bad = true;
         break;
       }
@@ -629,6 +630,33 @@ extern "C" mc_status mc_nlmc_build(mc_ctx* fine, const mc_nlmc_desc* d, mc_nlmc*
     cons.erase(std::unique(cons.begin(), cons.end()), cons.end());
     D.kc = (int32_t)cons.size();
     int b = 0;
+    // singularity check (exact, structural): every connected part of the region's graph
+    // needs a sink -- a connection leaving K_i^+ (zero Dirichlet) or a boundary term
+    UF luf(D.n);
+    std::vector<uint8_t> sink((size_t)D.n, 0);
+    for (int l = 0; l < D.n; ++l) {
+      const int32_t g = S[(size_t)l];
+      if (fs.ddiag[(size_t)g] > 0.0) sink[(size_t)l] = 1;
+      auto look = [&](int32_t h) {
+        const int32_t lh = loc[(size_t)h];
+        if (lh < 0) sink[(size_t)l] = 1;
+        else luf.u(l, lh);
+      };
+      for (int32_t e = arow[(size_t)g]; e < arow[(size_t)g + 1]; ++e) look(acol[(size_t)e]);
+      for (int32_t e = qrow[(size_t)g]; e < qrow[(size_t)g + 1]; ++e) look(qcol[(size_t)e]);
+    }
+    {
+      std::vector<uint8_t> rs((size_t)D.n, 0);
+      for (int l = 0; l < D.n; ++l)
+        if (sink[(size_t)l]) rs[(size_t)luf.f(l)] = 1;
+      for (int l = 0; l < D.n; ++l)
+        if (!rs[(size_t)luf.f(l)]) {
+          snprintf(msg, sizeof msg, "NLMC: local operator of coarse cell %d is not positive definite (a part of "
+                   "K_i^+ has no connection out of the region and no boundary term)", i);
+          delete nl;
+          return ctx_error(fine, MC_ERR_ARG, msg);
+        }
+    }
     for (int l = 0; l < D.n; ++l) {
       const int32_t g = S[(size_t)l];
       lglob.push_back(g);

@@ -120,3 +120,28 @@ def test_nlmc_gpu_model_accuracy():
     assert inv is not None
     cp.close()
     pb.close()
+
+
+def test_nlmc_errors():
+    """Argument and state errors of mc_nlmc_build (include/mc.h): coarse grid not dividing
+    the fine grid, a build after the first step, a region whose restricted operator is
+    singular (full oversampling of a no-flow problem without sinks)."""
+    from paper_2209_01158_b200 import Problem, MCError
+    scn = make_paper_analogue("2C", n=20, segments=3, lengths=(5, 12), seed=5)
+    for c in scn["continua"]:
+        c.pop("well_q", None)
+    pb = Problem(scn)
+    with pytest.raises(MCError) as e:
+        pb.nlmc(3, 3, 1)                                  # 20 % 3 != 0
+    assert "coarse grid" in str(e.value)
+    with pytest.raises(MCError) as e:
+        pb.nlmc(4, 4, 4)                                  # K_i^+ = whole no-flow domain
+    assert "not positive definite" in str(e.value)
+    sp_ = pb.nlmc(4, 4, 1)                                # valid after failures
+    assert sp_.n == sum(sp_.sizes) > 0
+    sp_.close()
+    pb.step("D")
+    with pytest.raises(MCError) as e:
+        pb.nlmc(4, 4, 1)
+    assert "after the first step" in str(e.value)
+    pb.close()

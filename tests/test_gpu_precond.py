@@ -43,3 +43,20 @@ def test_block_jacobi_parity(case, scheme, steps):
         _, its_j = _run(scn, scheme, steps, "jacobi")
         frac = len(scn["continua"]) - 1                     # the fracture network is the last continuum
         assert its_b[1:, frac].sum() < its_j[1:, frac].sum(), (its_b[:, frac], its_j[:, frac])
+
+
+def test_preconditioner_state_and_fallback():
+    """mc_set_preconditioner must precede mc_set_continuum; continua it does not apply to
+    (grids, CSR graphs with per-edge T) keep Jacobi and give the same trajectory."""
+    import ctypes as C
+    from paper_2209_01158_b200 import Problem, mc
+    scn = make(3)                                         # NLMC CSR graphs: not eligible
+    a, _ = _run(scn, "D", 3, "block")
+    b, _ = _run(scn, "D", 3, "jacobi")
+    for x, y in zip(a, b):
+        for u, v in zip(x, y):
+            assert np.array_equal(u, v)
+    pb = Problem(make(0))
+    assert pb.lib.mc_set_preconditioner(pb.ctx, 1) == mc.MC_ERR_STATE
+    assert pb.lib.mc_set_preconditioner(pb.ctx, 7) == mc.MC_ERR_ARG
+    pb.close()
