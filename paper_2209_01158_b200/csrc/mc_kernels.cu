@@ -1156,7 +1156,7 @@ __device__ __forceinline__ void bj_solve(const double* sl, double* zc, int lane)
   __syncwarp();
 }
 
-__device__ void run_group_bj(const StepParams& P, int g, int cl, double* x, const double* uo) {
+__device__ __noinline__ void run_group_bj(const StepParams& P, int g, int cl, double* x, const double* uo) {
   const Group& G = P.grp[g];
   const int W = G.cta_count * kWarps;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
