@@ -26,9 +26,10 @@
 
 #include "mc_nlmc.h"
 
+
 namespace mc {
 
-constexpr int kNlThreads = 256;      // one CTA per region K_i^+
+constexpr int kNlThreads = 512;      // max threads of the CTA that factors one region K_i^+
 constexpr int kWP = 8;               // cp.async prefetch distance (rows)
 constexpr int kNlMaxCons = 128;      // constraint rows per K_i^+ (4 per lane)
 constexpr int kNlSmemDoubles = 27000;   // 216 KB dynamic shared memory per CTA
@@ -78,10 +79,11 @@ __device__ __forceinline__ void nl_commit() { asm volatile("cp.async.commit_grou
 template <int N>
 __device__ __forceinline__ void nl_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
-__global__ void __launch_bounds__(kNlThreads) nlmc_basis_kernel(const NlParams P) {
+template <int NT>
+__global__ void __launch_bounds__(NT) nlmc_basis_kernel(const NlParams P) {
   extern __shared__ __align__(16) double sm[];
   const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
-  constexpr int NT = kNlThreads, NW = kNlThreads / 32;
+  constexpr int NW = NT / 32;
   double* ws = sm;
   double* band = P.band + (size_t)blockIdx.x * P.band_stride;
   double* Z = P.Z + (size_t)blockIdx.x * P.z_stride;
@@ -768,13 +770,17 @@ extern "C" mc_status mc_nlmc_build(mc_ctx* fine, const mc_nlmc_desc* d, mc_nlmc*
   P.wpb = wpb;
   P.spw = spw;
   const size_t smem = (size_t)wpb * spw * sizeof(double);
-  NL_CUDA(cudaFuncSetAttribute(nlmc_basis_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  // large regions (<= 2 per SM) take 512 threads, small ones 256 (measured)
+  const bool wide = per_sm <= 2;
+  if (wide) NL_CUDA(cudaFuncSetAttribute(nlmc_basis_kernel<512>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  else NL_CUDA(cudaFuncSetAttribute(nlmc_basis_kernel<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   cudaEvent_t e0, e1, e2;
   NL_CUDA(cudaEventCreate(&e0));
   NL_CUDA(cudaEventCreate(&e1));
   NL_CUDA(cudaEventCreate(&e2));
   NL_CUDA(cudaEventRecord(e0));
-  nlmc_basis_kernel<<<grid, kNlThreads, smem>>>(P);
+  if (wide) nlmc_basis_kernel<512><<<grid, 512, smem>>>(P);
+  else nlmc_basis_kernel<256><<<grid, 256, smem>>>(P);
   NL_CUDA(cudaGetLastError());
   NL_CUDA(cudaEventRecord(e1));
   int32_t herr = 0;
