@@ -399,6 +399,9 @@ __global__ void nlmc_project_kernel(const NlProj P) {
 using namespace mc;
 
 struct mc_nlmc {
+  ~mc_nlmc() {
+    if (d_dense) cudaFree(d_dense);
+  }
   std::string err;
   int L = 0;
   int64_t nH = 0, N = 0;
@@ -962,7 +965,6 @@ extern "C" mc_status mc_nlmc_times(const mc_nlmc* nl, double* ms_basis, double* 
 extern "C" const char* mc_nlmc_error_string(const mc_nlmc* nl) { return nl ? nl->err.c_str() : ""; }
 
 extern "C" mc_status mc_nlmc_destroy(mc_nlmc* nl) {
-  if (nl && nl->d_dense) cudaFree(nl->d_dense);
   delete nl;
   return MC_OK;
 }
