@@ -30,9 +30,10 @@ def _space_pair(kind, n, nH, m, segments=25, lengths=(120, 240), seed=32):
     from paper_2209_01158_b200 import Problem
     scn = make_paper_analogue(kind, n=n, segments=segments, lengths=lengths, seed=seed)
     sys_ = asm.assemble(scn)
-    ora = nlmc.build(scn, sys_, nH, nH, m)
+    hx, hy = (nH, nH) if np.ndim(nH) == 0 else nH
+    ora = nlmc.build(scn, sys_, hx, hy, m)
     pb = Problem(scn)
-    gpu = pb.nlmc(nH, nH, m)
+    gpu = pb.nlmc(hx, hy, m)
     return scn, sys_, ora, gpu, pb
 
 
@@ -47,7 +48,8 @@ def _perm(ora, gpu):
     return p
 
 
-@pytest.mark.parametrize("kind,n,nH,m", [("2C", 40, 8, 1), ("2C", 40, 8, 2), ("3C", 40, 8, 2), ("2C", 200, 20, 2)])
+@pytest.mark.parametrize("kind,n,nH,m", [("2C", 40, 8, 1), ("2C", 40, 8, 2), ("3C", 40, 8, 2), ("2C", 200, 20, 2),
+                                         ("2C", 40, (8, 5), 0), ("3C", 40, (5, 8), 1)])
 def test_nlmc_build_parity(kind, n, nH, m):
     seg, lens = (25, (120, 240)) if n == 200 else (6, (10, 30))
     scn, sys_, ora, gpu, pb = _space_pair(kind, n, nH, m, seg, lens)
