@@ -250,7 +250,10 @@ int32_t mc_abi_version(void);
  * (reading C31); u0bar = measure-weighted means.
  *
  * The fine context must have its continua and couplings set and no step taken yet (the
- * build reads the setup data); it is unchanged by the build.  Graph continua with fixed
+ * build reads the setup data); it is unchanged by the build.  The build runs on the
+ * context's device, is synchronous, and keeps its outputs in the mc_nlmc handle (the
+ * bases on the device) until mc_nlmc_destroy.  On failure *out is NULL and
+ * mc_error_string(fine) says why.  Graph continua with fixed
  * (Dirichlet) cells are not supported (MC_ERR_ARG).  A K_i^+ whose restricted operator
  * is singular (pure no-flow, K_i^+ = whole domain, no transfer sink) fails with
  * MC_ERR_ARG naming i.

@@ -1327,6 +1327,7 @@ mc_status export_fine(mc_ctx* c, const int32_t* const* host, FineSystem& fs) {
   if (c->finalized) return fail(c, MC_ERR_STATE, "NLMC build after the first step (setup data released)");
   fs = FineSystem();
   fs.L = c->L;
+  fs.device = c->opt.device;
   fs.off.assign((size_t)c->L + 1, 0);
   for (int a = 0; a < c->L; ++a) {
     const HostCont& H = c->hc[a];

@@ -720,9 +720,9 @@ extern "C" mc_status mc_nlmc_build(mc_ctx* fine, const mc_nlmc_desc* d, mc_nlmc*
     dom.push_back(D);
   }
   // ---- device: bases
-  int dev = 0, sms = 0;
-  NL_CUDA(cudaGetDevice(&dev));
-  NL_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  int sms = 0;
+  NL_CUDA(cudaSetDevice(fs.device));                  // the fine context's device
+  NL_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, fs.device));
   // one region per CTA; as many CTAs per SM as their shared memory allows (<= 8)
   const int spw = (int)((spw_need + 1) & ~int64_t(1));
   const int wpb = 1;

@@ -12,6 +12,7 @@ namespace mc {
 // caller's numbering, continua concatenated (global fine DOF g = off[alpha] + i).
 struct FineSystem {
   int L = 0;
+  int device = 0;                            // the context's CUDA device
   int nx = 0, ny = 0;                        // the grid every MC_GRID2D continuum lives on
   std::vector<int64_t> off;                  // [L + 1]
   std::vector<int32_t> kind;                 // [L] 0 grid, 1 graph
