@@ -60,3 +60,22 @@ def test_preconditioner_state_and_fallback():
     assert pb.lib.mc_set_preconditioner(pb.ctx, 1) == mc.MC_ERR_STATE
     assert pb.lib.mc_set_preconditioner(pb.ctx, 7) == mc.MC_ERR_ARG
     pb.close()
+
+
+def test_block_jacobi_run_matches_steps():
+    """mc_run (steps enqueued back to back, one sync) gives bitwise the per-step result."""
+    import torch
+    from paper_2209_01158_b200 import Problem
+    scn = make_paper_analogue("2C")
+    a = Problem(scn, precond="block")
+    reps = a.run("D", 5)
+    ra = [t.cpu().numpy() for t in a.state()]
+    b = Problem(scn, precond="block")
+    for _ in range(5):
+        b.step("D")
+    rb = [t.cpu().numpy() for t in b.state()]
+    for x, y in zip(ra, rb):
+        assert np.array_equal(x, y)
+    assert all(r["status"] == 0 for r in reps)
+    a.close()
+    b.close()
