@@ -1009,6 +1009,17 @@ static Plan make_plan(const mc_ctx* c, int scheme) {
       ctas[a] = std::min(useful_ctas(c->hc[a]), std::max(1, T / (2 * L)));
       used += ctas[a];
     }
+    // a block-Jacobi network needs one warp per 64-row chunk (resident layout): give it
+    // all its useful CTAs when they fit beside the others' shares, else it runs Jacobi
+    for (int a = 0; a < L; ++a)
+      if (c->tinv[a]) {
+        const int want = useful_ctas(c->hc[a]);
+        const int others = used - ctas[a];
+        if (want > ctas[a] && others + want <= T) {
+          used += want - ctas[a];
+          ctas[a] = want;
+        }
+      }
     int rest = std::max(0, T - used);
     // distribute by work, never beyond what a solve can use (latency-bound solves pay
     // for every extra CTA in their per-iteration barrier)
