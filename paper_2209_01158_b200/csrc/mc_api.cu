@@ -530,9 +530,65 @@ static void chain_order(const HostCont& H, std::vector<int32_t>& perm) {
 }
 
 // renumber every per-row array and the CSR of graph continuum H into chain order
+// Block-Jacobi (MC_PRECOND_BLOCK) packing: reorder the chains of `perm` (maximal runs of
+// connected consecutive cells) so that 64-cell chunks end where chains end: each chunk
+// is filled with the longest remaining chain that fits, the longest overall when none
+// does.  Fewer chain links cut by chunk boundaries = fewer CG iterations.
+static void pack_chains(const HostCont& H, std::vector<int32_t>& perm) {
+  const int64_t n = H.n;
+  auto linked = [&](int32_t a, int32_t b) {
+    for (int32_t e = H.rowptr[(size_t)a]; e < H.rowptr[(size_t)a + 1]; ++e)
+      if (H.col[(size_t)e] == b) return true;
+    return false;
+  };
+  std::vector<int64_t> start;
+  for (int64_t t = 0; t < n; ++t)
+    if (t == 0 || !linked(perm[(size_t)t - 1], perm[(size_t)t])) start.push_back(t);
+  start.push_back(n);
+  const int nc = (int)start.size() - 1;
+  // chains by length (longest first), ties in order of appearance
+  std::vector<std::vector<int>> bylen(65);          // 1..64; index 0 unused
+  std::vector<int> longer;                           // > 64, longest first
+  for (int c = 0; c < nc; ++c) {
+    const int64_t L = start[(size_t)c + 1] - start[(size_t)c];
+    if (L <= 64) bylen[(size_t)L].push_back(c);
+    else longer.push_back(c);
+  }
+  std::stable_sort(longer.begin(), longer.end(), [&](int x, int y) {
+    return start[(size_t)x + 1] - start[(size_t)x] > start[(size_t)y + 1] - start[(size_t)y];
+  });
+  for (auto& v : bylen) std::reverse(v.begin(), v.end());   // pop_back = first appearance
+  std::vector<int32_t> out;
+  out.reserve((size_t)n);
+  size_t li = 0;
+  while ((int64_t)out.size() < n) {
+    const int space = 64 - (int)(out.size() % 64);
+    int c = -1;
+    for (int L = space; L >= 1 && c < 0; --L)
+      if (!bylen[(size_t)L].empty()) {
+        c = bylen[(size_t)L].back();
+        bylen[(size_t)L].pop_back();
+      }
+    if (c < 0) {                                     // nothing fits: the longest chain left
+      if (li < longer.size()) {
+        c = longer[li++];
+      } else {
+        for (int L = 64; L >= 1 && c < 0; --L)
+          if (!bylen[(size_t)L].empty()) {
+            c = bylen[(size_t)L].back();
+            bylen[(size_t)L].pop_back();
+          }
+      }
+    }
+    for (int64_t t = start[(size_t)c]; t < start[(size_t)c + 1]; ++t) out.push_back(perm[(size_t)t]);
+  }
+  perm.swap(out);
+}
+
 static void apply_chain_order(HostCont& H) {
   const int64_t n = H.n;
   chain_order(H, H.perm);
+  if (H.bj) pack_chains(H, H.perm);
   H.inv.assign((size_t)n, 0);
   for (int64_t t = 0; t < n; ++t) H.inv[(size_t)H.perm[(size_t)t]] = (int32_t)t;
   auto pv = [&](std::vector<double>& v) {
