@@ -24,12 +24,12 @@ import numpy as np
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 
 
-def run_kind(kind, torch, Problem, make_paper_analogue):
+def run_kind(kind, torch, Problem, make_paper_analogue, precond="jacobi"):
     scn = make_paper_analogue(kind)
     NT = scn["NT"]
     rows, finals, curves = {}, {}, {}
     for scheme in ("coupled", "L", "D", "U"):
-        pb = Problem(scn)
+        pb = Problem(scn, precond=precond)
         u0 = [t.clone() for t in pb.state()]
         snaps = [[torch.empty_like(t) for t in u0] for _ in range(NT)]
         pb.run(scheme, NT)                                   # warm-up pass
@@ -79,11 +79,12 @@ def table(res):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--out", default="profiles/r01_paper_analogue")
+    ap.add_argument("--precond", default="jacobi", choices=["jacobi", "block"])
     args = ap.parse_args()
     import torch
     from inputs import make_paper_analogue
     from paper_2209_01158_b200 import Problem
-    res = [run_kind(k, torch, Problem, make_paper_analogue) for k in ("2C", "3C")]
+    res = [run_kind(k, torch, Problem, make_paper_analogue, args.precond) for k in ("2C", "3C")]
     md = "\n\n".join(table(r) for r in res)
     print(md)
     os.makedirs(os.path.dirname(args.out) or ".", exist_ok=True)
