@@ -1188,6 +1188,7 @@ static mc_status enqueue_step(mc_ctx* c, int scheme) {
         P.cont[a].resident = (nconts == 1 && nch <= (int64_t)kStages * G.cta_count * kWarps) ? 1 : 0;
         P.cont[a].bj = (nconts == 1 && nch <= (int64_t)G.cta_count * kWarps && c->tinv[a] != nullptr &&
                         scheme != MC_COUPLED) ? 1 : 0;
+        P.cont[a].bjs = (!P.cont[a].bj && nconts == 1 && c->tinv[a] != nullptr && scheme != MC_COUPLED) ? 1 : 0;
       }
   }
   for (int a = 0; a < c->L; ++a) {

@@ -1135,24 +1135,53 @@ __device__ __forceinline__ void group_allreduce(const StepParams& P, int g, int 
 //            published z, p_{j-1}), q = K p_j, partial p.q            -> alpha
 //   pass U:  x += alpha p_j, r -= alpha q, z = M^{-1} r, partials r.z, r.r -> beta, stop
 // The iterates solve the same SPD system; only the iteration count changes.
-__device__ __forceinline__ void bj_solve(const double* sl, double* zc, int lane) {
-  // z = M^{-1} r over the chunk: lane 0 sweeps (64 steps each way), rows in the slot
-  if (lane == 0) {
-    const double* r = sl + 2;
-    const double* inv = sl + 206;
-    const double* cp = zc + 64;
-    const double* em = zc + 128;
-    double dprev = 0.0;
-    for (int i = 0; i < 64; ++i) {
-      dprev = (r[i] - em[i] * dprev) * inv[i];
-      zc[i] = dprev;
-    }
-    double zn = zc[63];
-    for (int i = 62; i >= 0; --i) {
-      zn = __fma_rn(-cp[i], zn, zc[i]);
-      zc[i] = zn;
+
+// z = M^{-1} r over a 64-row chunk by the whole warp (lane l: rows 2l, 2l+1): both Thomas
+// sweeps are affine recurrences, d_i = (r_i - e_{i-1} d_{i-1}) / pivot_i forward and
+// z_i = d_i - c'_i z_{i+1} backward, evaluated as 5-level shuffle scans of the composed
+// affine maps instead of 64 serial steps each.
+__device__ __forceinline__ void bj_scan_solve(const double* r, const double* inv, const double* cp,
+                                              const double* em, int lane, double& z0, double& z1) {
+  const int i0 = 2 * lane, i1 = i0 + 1;
+  // forward: d_i = a_i d_{i-1} + b_i
+  const double a0 = -em[i0] * inv[i0], b0 = r[i0] * inv[i0];
+  const double a1 = -em[i1] * inv[i1], b1 = r[i1] * inv[i1];
+  double A = a1 * a0, B = __fma_rn(a1, b0, b1);
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    const double Ap = __shfl_up_sync(0xffffffffu, A, off), Bp = __shfl_up_sync(0xffffffffu, B, off);
+    if (lane >= off) {
+      B = __fma_rn(A, Bp, B);
+      A = A * Ap;
     }
   }
+  double dprev = __shfl_up_sync(0xffffffffu, B, 1);     // d_{2l-1}
+  if (lane == 0) dprev = 0.0;
+  const double d0 = __fma_rn(a0, dprev, b0), d1 = B;
+  // backward: z_i = g_i z_{i+1} + h_i, g = -c', h = d
+  const double g0 = -cp[i0], g1 = -cp[i1];
+  double Ab = g0 * g1, Bb = __fma_rn(g0, d1, d0);
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    const double An = __shfl_down_sync(0xffffffffu, Ab, off), Bn = __shfl_down_sync(0xffffffffu, Bb, off);
+    if (lane + off < 32) {
+      Bb = __fma_rn(Ab, Bn, Bb);
+      Ab = Ab * An;
+    }
+  }
+  double znext = __shfl_down_sync(0xffffffffu, Bb, 1);  // z_{2l+2}
+  if (lane == 31) znext = 0.0;
+  z0 = Bb;
+  z1 = __fma_rn(g1, znext, d1);
+}
+
+__device__ __forceinline__ void bj_solve(const double* sl, double* zc, int lane) {
+  // z = M^{-1} r over the chunk (r at sl + 2, 1/pivot at sl + 206, c' at zc + 64, e at zc + 128)
+  double z0, z1;
+  bj_scan_solve(sl + 2, sl + 206, zc + 64, zc + 128, lane, z0, z1);
+  __syncwarp();
+  zc[2 * lane] = z0;
+  zc[2 * lane + 1] = z1;
   __syncwarp();
 }
 
@@ -1369,6 +1398,288 @@ __device__ __noinline__ void run_group_bj(const StepParams& P, int g, int cl, do
   }
 }
 
+
+// ---------------------------------------------------------------- streaming block-Jacobi (bjs)
+// The block-Jacobi PCG of run_group_bj for networks too large to stay resident (configs
+// 2 and 4): both passes stream 64-row chunks round-robin over the group's warps, TMA
+// staging one chunk ahead (as iter_ells).
+//   pass U:  x += alpha p, r -= alpha q, z = M^{-1} r (in-chunk Thomas), r.z, r.r
+//   pass S:  p = z + beta p_old on the chunk's 68-row window and its far neighbours
+//            (gathered z, p_old), q = K p, p.q
+// r, q, z single buffers (each written and read by the owner, z read by neighbours only
+// after the reduction); p double-buffered (neighbours read p_old while owners write p).
+__device__ void bjs_pass_u(const StepParams& P, const ContDev& C, int wg, int W, const Stage& st, double* x,
+                           const double* pj, double* zg, double* pzero, double alpha, double (&a2)[2]) {
+  const int lane = threadIdx.x & 31;
+  double* wsm = st.wsm;
+  const int64_t off = C.off;
+  const int r1 = (int)C.n, nch = (r1 + 63) / 64;
+  auto tix = [&](int m) { return (m / W) & 1; };
+  auto prefetch = [&](int m) {
+    const int t = tix(m);
+    double* sl = wsm + t * kSlotE;
+    __syncwarp();
+    if (lane == 0) {
+      const int64_t g = off + 64 * (int64_t)m;
+      st.begin(t, 7u * 512u);
+      uint64_t* bar = st.bars + t;
+      bulk_g2s(sl + 0, P.r[0] + g, 512, bar);
+      bulk_g2s(sl + 64, P.q[0] + g, 512, bar);
+      bulk_g2s(sl + 128, pj + g, 512, bar);
+      bulk_g2s(sl + 192, x + g, 512, bar);
+      bulk_g2s(sl + 256, C.tinv + g, 512, bar);
+      bulk_g2s(sl + 320, C.tcp + g, 512, bar);
+      bulk_g2s(sl + 384, C.tem + g, 512, bar);
+    }
+  };
+  if (wg >= nch) return;
+  prefetch(wg);
+  for (int m = wg; m < nch; m += W) {
+    if (m + W < nch) prefetch(m + W);
+    const int t = tix(m);
+    st.wait(t);
+    double* sl = wsm + t * kSlotE;
+    const int base = 64 * m + 2 * lane;
+    const int64_t g = off + base;
+    double rn[2], xn[2];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int l2 = 2 * lane + h;
+      xn[h] = __fma_rn(alpha, sl[128 + l2], sl[192 + l2]);
+      rn[h] = __fma_rn(-alpha, sl[64 + l2], sl[0 + l2]);
+    }
+    __syncwarp();
+    sl[2 * lane] = rn[0];
+    sl[2 * lane + 1] = rn[1];
+    __syncwarp();
+    {                                                   // z = M^{-1} r over the chunk
+      double z0, z1;
+      bj_scan_solve(sl, sl + 256, sl + 320, sl + 384, lane, z0, z1);
+      sl[448 + 2 * lane] = z0;
+      sl[449 + 2 * lane] = z1;
+    }
+    __syncwarp();
+#pragma unroll
+    for (int h = 0; h < 2; ++h)
+      if (base + h < r1) {
+        const double zv = sl[448 + 2 * lane + h];
+        x[g + h] = xn[h];
+        stmut(P.r[0] + g + h, rn[h]);
+        stmut(zg + g + h, zv);
+        if (pzero) stmut(pzero + g + h, 0.0);
+        a2[0] += rn[h] * zv;
+        a2[1] += rn[h] * rn[h];
+      }
+  }
+}
+
+__device__ void bjs_pass_s(const StepParams& P, const ContDev& C, int wg, int W, const Stage& st,
+                           const double* zg, const double* pold, double* pnew_g, double beta, double (&a1)[1]) {
+  const int lane = threadIdx.x & 31;
+  double* wsm = st.wsm;
+  double* pnb = wsm + kWarpSmem - kPnBuf;
+  const int64_t off = C.off, es = C.estride;
+  const int r1 = (int)C.n, nch = (r1 + 63) / 64;
+  auto tix = [&](int m) { return (m / W) & 1; };
+  auto prefetch = [&](int m) {
+    const int t = tix(m);
+    double* sl = wsm + t * kSlotE;
+    __syncwarp();
+    if (lane == 0) {
+      const int64_t b = 64 * (int64_t)m;
+      const int64_t g = off + b;
+      const bool full = g >= 2;
+      const unsigned wb = full ? 544u : 528u;
+      st.begin(t, 2u * wb + 512u + 4u * 256u);
+      uint64_t* bar = st.bars + t;
+      const int64_t g0 = g - (full ? 2 : 0);
+      const int d0 = full ? 0 : 2;
+      bulk_g2s(sl + d0, zg + g0, wb, bar);
+      bulk_g2s(sl + 68 + d0, pold + g0, wb, bar);
+      bulk_g2s(sl + 136, P.dsD + g, 512, bar);
+      int32_t* si = reinterpret_cast<int32_t*>(sl + 200);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) bulk_g2s(si + k * 64, C.ecol + k * es + b, 256, bar);
+    }
+  };
+  if (wg >= nch) return;
+  prefetch(wg);
+  for (int m = wg; m < nch; m += W) {
+    if (m + W < nch) prefetch(m + W);
+    const int t = tix(m);
+    st.wait(t);
+    const double* sl = wsm + t * kSlotE;
+    const int base = 64 * m + 2 * lane;
+    const int64_t g = off + base;
+    const bool ok0 = base < r1, ok1 = base + 1 < r1;
+    // codes and far gathers (z, p_old of rows outside the window)
+    int32_t j[2][4];
+    {
+      const int32_t* si = reinterpret_cast<const int32_t*>(sl + 200);
+#pragma unroll
+      for (int h = 0; h < 2; ++h)
+#pragma unroll
+        for (int k = 0; k < 4; ++k) j[h][k] = si[k * 64 + 2 * lane + h];
+    }
+    int fs0 = -1, fs1 = -1, fs2 = -1, fs3 = -1;
+    int32_t i0 = -1, i1 = -1, i2 = -1, i3 = -1;
+    int nfar = 0;
+#pragma unroll
+    for (int h = 0; h < 2; ++h)
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+        if (j[h][k] >= 0) {
+          if (nfar == 0) { i0 = j[h][k]; fs0 = 4 * h + k; }
+          else if (nfar == 1) { i1 = j[h][k]; fs1 = 4 * h + k; }
+          else if (nfar == 2) { i2 = j[h][k]; fs2 = 4 * h + k; }
+          else if (nfar == 3) { i3 = j[h][k]; fs3 = 4 * h + k; }
+          ++nfar;
+        }
+    double w0 = 0.0, w1 = 0.0, w2 = 0.0, w3 = 0.0;
+    if (i0 >= 0) w0 = __fma_rn(beta, ldnb(pold + i0), ldnb(zg + i0));
+    if (i1 >= 0) w1 = __fma_rn(beta, ldnb(pold + i1), ldnb(zg + i1));
+    if (i2 >= 0) w2 = __fma_rn(beta, ldnb(pold + i2), ldnb(zg + i2));
+    if (i3 >= 0) w3 = __fma_rn(beta, ldnb(pold + i3), ldnb(zg + i3));
+    // p on the window (own rows and the 2-row halos)
+    double pc[2];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int w = 2 + 2 * lane + h;
+      pc[h] = __fma_rn(beta, sl[68 + w], sl[w]);
+    }
+    __syncwarp();
+    pnb[2 + 2 * lane] = pc[0];
+    pnb[3 + 2 * lane] = pc[1];
+    if (lane < 4) {
+      const int w = lane < 2 ? lane : 64 + lane;
+      pnb[w] = __fma_rn(beta, sl[68 + w], sl[w]);
+    }
+    if (ok1) st2mut(pnew_g + g, make_double2(pc[0], pc[1]));
+    else if (ok0) stmut(pnew_g + g, pc[0]);
+    __syncwarp();
+    double qv[2];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      double sum = 0.0;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const int32_t cd = j[h][k];
+        double v = pc[h];
+        if (cd <= -2) v = pnb[-2 - cd];
+        else if (cd >= 0) {
+          if (fs0 == 4 * h + k) v = w0;
+          else if (fs1 == 4 * h + k) v = w1;
+          else if (fs2 == 4 * h + k) v = w2;
+          else if (fs3 == 4 * h + k) v = w3;
+          else v = __fma_rn(beta, ldnb(pold + cd), ldnb(zg + cd));     // rare: > 4 far
+        }
+        sum += pc[h] - v;
+      }
+      qv[h] = sl[136 + 2 * lane + h] * pc[h] + C.Tconst * sum;
+    }
+    if (ok1) st2mut(P.q[0] + g, make_double2(qv[0], qv[1]));
+    else if (ok0) stmut(P.q[0] + g, qv[0]);
+    if (ok0) a1[0] += pc[0] * qv[0];
+    if (ok1) a1[0] += pc[1] * qv[1];
+  }
+}
+
+__device__ __noinline__ void run_group_bjs(const StepParams& P, int g, int cl, double* x, const double* uo) {
+  const Group& G = P.grp[g];
+  const int W = G.cta_count * kWarps;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int wg = cl * kWarps + wid;
+  const bool leader = (cl == 0 && threadIdx.x == 0);
+  const long long t0 = leader ? globaltimer() : 0;
+  const int ca = __ffs(G.cont_mask) - 1;
+  const ContDev& C = P.cont[ca];
+  extern __shared__ __align__(16) double dsm[];
+  Stage st;
+  st.wsm = dsm + wid * kWarpSmem;
+  st.bars = reinterpret_cast<uint64_t*>(dsm + kWarps * kWarpSmem) + wid * kNBars;
+  st.ph = reinterpret_cast<unsigned*>(dsm + kWarps * kWarpSmem + kWarps * kNBars) + 2 * wid;
+  const int r1 = (int)C.n;
+  double* zg = P.q[1];
+  double a3[3] = {0.0, 0.0, 0.0};
+  for (int mm = wg; 32 * mm < r1; mm += W) {
+    Item rit{};
+    rit.cont = ca;
+    rit.kind = ITEM_GRAPH;
+    rit.a = 32 * mm;
+    rit.b = min(32 * mm + 32, r1);
+    init_item<false>(P, rit, uo, x, G.phase, a3);
+  }
+  unsigned long long epoch = 0;
+  double t3[3];
+  group_allreduce<3>(P, g, cl, epoch, a3, t3);
+  const double bb = t3[0];
+  double rr = t3[1];
+  int64_t iters = 0;
+  int status = MC_OK;
+  bool zero = false;
+  if (bb == 0.0) {
+    zero = true;
+    rr = 0.0;
+  } else if (!(rr <= G.tol2 * bb)) {
+    fence_proxy_async_shared_global();
+    double rz;
+    {
+      double a2[2] = {0.0, 0.0};
+      bjs_pass_u(P, C, wg, W, st, x, P.p[0], zg, P.p[1], 0.0, a2);     // U_0: z_0, p_{-1} = 0
+      double t2[2];
+      group_allreduce<2>(P, g, cl, epoch, a2, t2);
+      rz = t2[0];
+    }
+    double beta = 0.0;
+    for (int64_t j = 0;; ++j) {
+      double* pj = P.p[j & 1];
+      const double* pold = P.p[(j + 1) & 1];
+      double a1[1] = {0.0};
+      fence_proxy_async_shared_global();
+      bjs_pass_s(P, C, wg, W, st, zg, pold, pj, beta, a1);
+      double t1[1];
+      group_allreduce<1>(P, g, cl, epoch, a1, t1);
+      if (!(t1[0] > 0.0)) {
+        iters = j;
+        status = MC_ERR_BREAKDOWN;
+        break;
+      }
+      const double alpha = rz / t1[0];
+      double a2[2] = {0.0, 0.0};
+      fence_proxy_async_shared_global();
+      bjs_pass_u(P, C, wg, W, st, x, pj, zg, nullptr, alpha, a2);
+      double t2[2];
+      group_allreduce<2>(P, g, cl, epoch, a2, t2);
+      rr = t2[1];
+      iters = j + 1;
+      if (rr <= G.tol2 * bb) break;
+      if (j + 1 >= G.maxit) {
+        status = MC_ERR_NOCONV;
+        break;
+      }
+      if (!(t2[0] > 0.0)) {
+        status = MC_ERR_BREAKDOWN;
+        break;
+      }
+      beta = t2[0] / rz;
+      rz = t2[0];
+    }
+  }
+  if (zero)
+    for (int64_t i = (int64_t)wg * 32 + lane; i < C.n; i += (int64_t)W * 32) x[C.off + i] = 0.0;
+  if (leader) {
+    GroupOut o;
+    o.iters = iters;
+    o.status = status;
+    o.pad = 0;
+    o.bb = bb;
+    o.rr = rr;
+    o.t0 = t0;
+    o.t1 = globaltimer();
+    P.gout[g] = o;
+  }
+}
+
 // ---------------------------------------------------------------- the step kernel
 template <bool CPL>
 __device__ void run_group(const StepParams& P, int g, int cl, double* x, const double* uo) {
@@ -1537,6 +1848,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) step_kernel(const __grid
         const int a0 = __ffs(G.cont_mask) - 1;
         if (P.coupled) run_group<true>(P, g, cl, x, uo);
         else if ((G.cont_mask & (G.cont_mask - 1)) == 0 && P.cont[a0].bj) run_group_bj(P, g, cl, x, uo);
+        else if ((G.cont_mask & (G.cont_mask - 1)) == 0 && P.cont[a0].bjs) run_group_bjs(P, g, cl, x, uo);
         else run_group<false>(P, g, cl, x, uo);
       }
       if (ph + 1 < P.nphases) grid_barrier(P, (unsigned long long)(ph + 1) * gridDim.x);
