@@ -91,17 +91,21 @@ def workload_name(cid, scheme):
 
 
 # ------------------------------------------------------------------ algorithmic bytes
-def step_bytes(pb, rep, scheme):
+def step_bytes(pb, rep, scheme, precond="jacobi"):
     """Algorithmic HBM bytes of one step kernel: per CG iteration every
     row reads x, r, q, p, D^-1 and its shift, writes x, r, p, q once; grid rows read
     Tx, Ty; graph rows read their row pointer and column indices (values when not
     uniform).  Init pass: ~76 B/row + 16 B per transfer entry.  Neighbour gathers are
-    cache hits and not counted."""
+    cache hits and not counted.  Block-Jacobi networks (precond "block", §5.2c) make two
+    passes per iteration: U reads r, q, p, x and the three Thomas factors, writes x, r, z
+    (80 B); S reads z, p_old, shift and 16 B of codes, writes p, q (56 B)."""
     sizes, kinds, nnz_off = pb.byte_model
     total = 0.0
     iters = rep["iters"]
     for a, n in enumerate(sizes):
         per = 96.0 if kinds[a] == "grid" else 84.0 + nnz_off[a]
+        if precond == "block" and kinds[a] != "grid" and scheme != "coupled":
+            per = 136.0
         it = iters[0] if scheme == "coupled" else iters[a]
         total += it * per * n + 76.0 * n
     return total
@@ -297,7 +301,7 @@ def main():
     total_ms = max_over_ranks(sum(step_ms), world)
     value = aggregate(world, dof, args.steps, total_ms)
     # roofline of the dominant (only) kernel: the step kernel, one launch per step
-    bytes_per = sum(step_bytes(pb, r, args.scheme) for r in reps) / args.steps
+    bytes_per = sum(step_bytes(pb, r, args.scheme, args.precond) for r in reps) / args.steps
     kern_ms = sum(r["ms"] for r in reps) / args.steps
     peak, peak_src = peaks()
     achieved = bytes_per / (kern_ms * 1e-3) / 1e9

@@ -14,6 +14,8 @@ timeout 600 python bench.py --config 0 --steps 20 --warmup 3 > $R/bench_config0.
 timeout 1200 python bench.py --config 2 --steps 2 --warmup 3 --no-cpu-baseline > $R/bench_config2.json 2> $R/bench_config2.err
 timeout 900 python bench.py --config 3 --steps 10 --warmup 3 > $R/bench_config3.json 2> $R/bench_config3.err
 timeout 1500 python bench.py --config 4 --steps 2 --warmup 3 --no-cpu-baseline > $R/bench_config4.json 2> $R/bench_config4.err
+timeout 900 python bench.py --config 2 --steps 2 --warmup 3 --no-cpu-baseline --precond block > $R/bench_config2_block.json 2> $R/bench_config2_block.err
+timeout 1500 python bench.py --config 4 --steps 2 --warmup 3 --no-cpu-baseline --precond block > $R/bench_config4_block.json 2> $R/bench_config4_block.err
 timeout 600 python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-e2e > $R/plain.json 2>&1 && \
 timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv \
   --log-file $R/launches_config1.csv python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-e2e > $R/ncu_launch.log 2>&1
@@ -22,5 +24,6 @@ timeout 900 ncu --set full --clock-control none --import-source on -k regex:step
   python scripts/prof_step.py 4 D 40 1 > $R/prof4_ncu.log 2>&1
 timeout 600 python scripts/nlmc_bench.py --oracle --out $R/nlmc.json > $R/nlmc.log 2>&1
 timeout 600 python scripts/paper_analogue.py --out $R/paper_analogue > $R/paper_analogue.log 2>&1
+timeout 600 python scripts/paper_analogue.py --precond block --out $R/paper_analogue_block > $R/paper_analogue_block.log 2>&1
 timeout 600 python scripts/coupled_cfg4.py 400 --out $R/coupled_config4_capped.json > $R/coupled_cfg4.log 2>&1
 cat $R/pytest_gpu.log
