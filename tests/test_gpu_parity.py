@@ -67,12 +67,13 @@ def assert_parity(got, ref, tol=TOL):
 
 
 # ---------------------------------------------------------------- worked example
-def _one_cell(torch, scheme):
+def _one_cell(torch, scheme, precond=0):
     from paper_2209_01158_b200 import mc
     lib = mc.load()
     ctx = C.c_void_p()
     opt = mc.mc_options(tau=1.0, rtol=1e-12, stream=C.c_void_p(torch.cuda.current_stream().cuda_stream))
     assert lib.mc_create(C.byref(ctx), 2, C.byref(opt)) == 0
+    assert lib.mc_set_preconditioner(ctx, precond) == 0
     keep = []
     for a, u0 in enumerate((1.0, 0.0)):
         arr = np.array([u0])
@@ -95,6 +96,9 @@ def _one_cell(torch, scheme):
 def test_worked_example_one_cell(torch_cuda):
     assert np.allclose(_one_cell(torch_cuda, "coupled"), [2 / 3, 1 / 3], rtol=1e-14, atol=1e-15)
     assert np.allclose(_one_cell(torch_cuda, "D"), [0.5, 0.5], rtol=1e-14, atol=1e-15)
+    # block-Jacobi on one-cell graph continua (one chunk, no links): the same values
+    assert np.allclose(_one_cell(torch_cuda, "coupled", 1), [2 / 3, 1 / 3], rtol=1e-14, atol=1e-15)
+    assert np.allclose(_one_cell(torch_cuda, "D", 1), [0.5, 0.5], rtol=1e-14, atol=1e-15)
 
 
 # ---------------------------------------------------------------- full trajectories
