@@ -97,15 +97,15 @@ def step_bytes(pb, rep, scheme, precond="jacobi"):
     Tx, Ty; graph rows read their row pointer and column indices (values when not
     uniform).  Init pass: ~76 B/row + 16 B per transfer entry.  Neighbour gathers are
     cache hits and not counted.  Block-Jacobi networks (precond "block", §5.2c) make two
-    passes per iteration: U reads r, q, p, x and the three Thomas factors, writes x, r, z
-    (80 B); S reads z, p_old, shift and 16 B of codes, writes p, q (56 B)."""
+    passes per iteration: U reads r, q, p, x and two Thomas factors (1/pivot, e; c' is
+    recomputed), writes x, r, z (72 B); S reads z, p_old, shift and 16 B of codes, writes p, q (56 B)."""
     sizes, kinds, nnz_off = pb.byte_model
     total = 0.0
     iters = rep["iters"]
     for a, n in enumerate(sizes):
         per = 96.0 if kinds[a] == "grid" else 84.0 + nnz_off[a]
         if precond == "block" and kinds[a] != "grid" and scheme != "coupled":
-            per = 136.0
+            per = 128.0
         it = iters[0] if scheme == "coupled" else iters[a]
         total += it * per * n + 76.0 * n
     return total

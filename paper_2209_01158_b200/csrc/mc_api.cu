@@ -864,7 +864,7 @@ static mc_status finalize(mc_ctx* c) {
               const double ei = (i + 1 < i1 && linked(i)) ? -H.Tconst : 0.0;
               inv[gi] = 1.0 / den;
               em[gi] = eprev;
-              cprev = ei / den;
+              cprev = ei * inv[gi];                   // = em[i+1] * inv[i]: bjs recomputes it
               cpv[gi] = cprev;
               eprev = ei;
             }

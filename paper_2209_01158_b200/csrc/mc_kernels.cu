@@ -1158,8 +1158,10 @@ __device__ __forceinline__ void bj_scan_solve(const double* r, const double* inv
   double dprev = __shfl_up_sync(0xffffffffu, B, 1);     // d_{2l-1}
   if (lane == 0) dprev = 0.0;
   const double d0 = __fma_rn(a0, dprev, b0), d1 = B;
-  // backward: z_i = g_i z_{i+1} + h_i, g = -c', h = d
-  const double g0 = -cp[i0], g1 = -cp[i1];
+  // backward: z_i = g_i z_{i+1} + h_i, g = -c', h = d.  cp == nullptr: c'_i = e_i / pivot_i
+  // recomputed as em[i+1] * inv[i] (bitwise the stored factor; e_63 = 0 at the chunk's end)
+  const double g0 = cp ? -cp[i0] : -(em[i1] * inv[i0]);
+  const double g1 = cp ? -cp[i1] : (lane == 31 ? -0.0 : -(em[i1 + 1] * inv[i1]));
   double Ab = g0 * g1, Bb = __fma_rn(g0, d1, d0);
 #pragma unroll
   for (int off = 1; off < 32; off <<= 1) {
@@ -1403,7 +1405,8 @@ __device__ __noinline__ void run_group_bj(const StepParams& P, int g, int cl, do
 // The block-Jacobi PCG of run_group_bj for networks too large to stay resident (configs
 // 2 and 4): both passes stream 64-row chunks round-robin over the group's warps, TMA
 // staging one chunk ahead (as iter_ells).
-//   pass U:  x += alpha p, r -= alpha q, z = M^{-1} r (in-chunk Thomas), r.z, r.r
+//   pass U:  x += alpha p, r -= alpha q, z = M^{-1} r (in-chunk Thomas from 1/pivot and e;
+//            c' recomputed), r.z, r.r
 //   pass S:  p = z + beta p_old on the chunk's 68-row window and its far neighbours
 //            (gathered z, p_old), q = K p, p.q
 // r, q, z single buffers (each written and read by the owner, z read by neighbours only
@@ -1421,15 +1424,14 @@ __device__ void bjs_pass_u(const StepParams& P, const ContDev& C, int wg, int W,
     __syncwarp();
     if (lane == 0) {
       const int64_t g = off + 64 * (int64_t)m;
-      st.begin(t, 7u * 512u);
+      st.begin(t, 6u * 512u);
       uint64_t* bar = st.bars + t;
       bulk_g2s(sl + 0, P.r[0] + g, 512, bar);
       bulk_g2s(sl + 64, P.q[0] + g, 512, bar);
       bulk_g2s(sl + 128, pj + g, 512, bar);
       bulk_g2s(sl + 192, x + g, 512, bar);
       bulk_g2s(sl + 256, C.tinv + g, 512, bar);
-      bulk_g2s(sl + 320, C.tcp + g, 512, bar);
-      bulk_g2s(sl + 384, C.tem + g, 512, bar);
+      bulk_g2s(sl + 384, C.tem + g, 512, bar);       // c' recomputed from e and 1/pivot
     }
   };
   if (wg >= nch) return;
@@ -1454,7 +1456,7 @@ __device__ void bjs_pass_u(const StepParams& P, const ContDev& C, int wg, int W,
     __syncwarp();
     {                                                   // z = M^{-1} r over the chunk
       double z0, z1;
-      bj_scan_solve(sl, sl + 256, sl + 320, sl + 384, lane, z0, z1);
+      bj_scan_solve(sl, sl + 256, nullptr, sl + 384, lane, z0, z1);
       sl[448 + 2 * lane] = z0;
       sl[449 + 2 * lane] = z1;
     }
