@@ -32,9 +32,14 @@ constexpr int kSlotG = 536;            // grid strip slot: 8 arrays x 64 doubles
 constexpr int kSlotE = 528;            // ELL chunk slot: r, q, p, D^-1 windows (68), x, shift (64), 4 x 64 int32 codes
 constexpr int kStagesE = 2;                // ELL pass: chunk in flight + chunk computed
 constexpr int kPnBuf = 72;                 // ELL pass: new p of the chunk window (68) per warp
-constexpr int kWarpSmem = ((kStages * kSlotG > kStagesE * kSlotE) ? kStages * kSlotG : kStagesE * kSlotE) + kPnBuf;
+#ifndef MC_BJS_STAGES
+#define MC_BJS_STAGES 2
+#endif
+constexpr int kStagesB = MC_BJS_STAGES;    // streaming block-Jacobi passes: chunks in flight + 1
+constexpr int kStagesEB = (kStagesE > kStagesB) ? kStagesE : kStagesB;
+constexpr int kWarpSmem = ((kStages * kSlotG > kStagesEB * kSlotE) ? kStages * kSlotG : kStagesEB * kSlotE) + kPnBuf;
 // bytes per CTA: staging slots, then one mbarrier per slot per warp, then a parity word per warp
-constexpr int kNBars = (kStages > kStagesE) ? kStages : kStagesE;   // mbarriers per warp
+constexpr int kNBars = (kStages > kStagesEB) ? kStages : kStagesEB;   // mbarriers per warp
 constexpr int kDynSmem = kWarps * kWarpSmem * 8 + kWarps * kNBars * 8 + kWarps * 8;
 
 enum ContKind : int32_t { KIND_GRID = 0, KIND_GRAPH = 1 };

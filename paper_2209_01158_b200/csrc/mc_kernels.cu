@@ -1404,7 +1404,7 @@ __device__ __noinline__ void run_group_bj(const StepParams& P, int g, int cl, do
 // ---------------------------------------------------------------- streaming block-Jacobi (bjs)
 // The block-Jacobi PCG of run_group_bj for networks too large to stay resident (configs
 // 2 and 4): both passes stream 64-row chunks round-robin over the group's warps, TMA
-// staging one chunk ahead (as iter_ells).
+// staging kStagesB - 1 chunks ahead (MC_BJS_STAGES).
 //   pass U:  x += alpha p, r -= alpha q, z = M^{-1} r (in-chunk Thomas from 1/pivot and e;
 //            c' recomputed), r.z, r.r
 //   pass S:  p = z + beta p_old on the chunk's 68-row window and its far neighbours
@@ -1417,7 +1417,7 @@ __device__ void bjs_pass_u(const StepParams& P, const ContDev& C, int wg, int W,
   double* wsm = st.wsm;
   const int64_t off = C.off;
   const int r1 = (int)C.n, nch = (r1 + 63) / 64;
-  auto tix = [&](int m) { return (m / W) & 1; };
+  auto tix = [&](int m) { return (m / W) % kStagesB; };
   auto prefetch = [&](int m) {
     const int t = tix(m);
     double* sl = wsm + t * kSlotE;
@@ -1435,9 +1435,11 @@ __device__ void bjs_pass_u(const StepParams& P, const ContDev& C, int wg, int W,
     }
   };
   if (wg >= nch) return;
-  prefetch(wg);
+#pragma unroll
+  for (int k = 0; k < kStagesB - 1; ++k)
+    if (wg + k * W < nch) prefetch(wg + k * W);
   for (int m = wg; m < nch; m += W) {
-    if (m + W < nch) prefetch(m + W);
+    if (m + (kStagesB - 1) * W < nch) prefetch(m + (kStagesB - 1) * W);
     const int t = tix(m);
     st.wait(t);
     double* sl = wsm + t * kSlotE;
@@ -1482,7 +1484,7 @@ __device__ void bjs_pass_s(const StepParams& P, const ContDev& C, int wg, int W,
   double* pnb = wsm + kWarpSmem - kPnBuf;
   const int64_t off = C.off, es = C.estride;
   const int r1 = (int)C.n, nch = (r1 + 63) / 64;
-  auto tix = [&](int m) { return (m / W) & 1; };
+  auto tix = [&](int m) { return (m / W) % kStagesB; };
   auto prefetch = [&](int m) {
     const int t = tix(m);
     double* sl = wsm + t * kSlotE;
@@ -1505,9 +1507,11 @@ __device__ void bjs_pass_s(const StepParams& P, const ContDev& C, int wg, int W,
     }
   };
   if (wg >= nch) return;
-  prefetch(wg);
+#pragma unroll
+  for (int k = 0; k < kStagesB - 1; ++k)
+    if (wg + k * W < nch) prefetch(wg + k * W);
   for (int m = wg; m < nch; m += W) {
-    if (m + W < nch) prefetch(m + W);
+    if (m + (kStagesB - 1) * W < nch) prefetch(m + (kStagesB - 1) * W);
     const int t = tix(m);
     st.wait(t);
     const double* sl = wsm + t * kSlotE;
