@@ -14,8 +14,13 @@ assemble  Eq. app-md / app-tc / app-mc assembly of M, A = D +
 schemes   coupled backward Euler, Eq. ct-mc, and the decoupled
           D-scheme, Eq. si-mc with A0 = blockdiag(A) (PAPER.md:446-486), solved
           with SciPy sparse LU (SuperLU) factorisations, or plain Jacobi-PCG.
-cg        a plain Jacobi-preconditioned CG used where a sparse
-          factorisation is infeasible (config 4) and for the CG unit pins.
+cg        a plain Jacobi-preconditioned CG in NumPy, for the CG
+          unit pins.
+flux_pcg.c / fluxcg
+          plain C + OpenMP Jacobi-PCG on the unassembled flux-form operator and the
+          coupled / D-scheme steppers built on it (relres 1e-13), for the sizes a
+          sparse factorisation cannot take (configs 2 and 4); the
+          C library is compiled on first use (gcc) or by __graft_entry__.build().
 
 Every function is pinned by ``tests/test_oracle_*.py`` against closed forms,
 brute force and the paper's / SPEC's worked examples.

@@ -123,6 +123,21 @@ def grid_continuum(nx, ny, h, k, c, dirichlet):
     return sp.csr_matrix(D), M, F
 
 
+def grid_dirichlet_source(nx, ny, h, k, dirichlet):
+    """F of a grid continuum: T_b g on the Dirichlet columns (C3), as grid_continuum."""
+    N = nx * ny
+    F = np.zeros(N)
+    if dirichlet is None:
+        return F
+    kk = np.full(N, float(k)) if np.ndim(k) == 0 else np.asarray(k, dtype=np.float64)
+    for col, g in ((0, dirichlet[0]), (nx - 1, dirichlet[1])):
+        if g is None:
+            continue
+        cells = np.arange(col, N, nx)
+        F[cells] += kk[cells] * h / (h / 2.0) * float(g)
+    return F
+
+
 def fracture_continuum(n, h, cells, edges, k_f, c_f):
     """1D fracture continuum: T_f = k_f |E|/d with |E| = 1, d = h (C7); m = c_f h (C1)."""
     Nf = len(cells)
@@ -228,6 +243,53 @@ def apply_dirichlet_rows(sys: System, mask, g) -> System:
     return System(sys.sizes, M, A, F, u0, sys.names)
 
 
+class FluxSystem(System):
+    """M, F, u0 and the flux form of a fine-grid scenario WITHOUT the assembled A
+    (configs 2 and 4: nnz(A) up to 4e8).  Used by the CG oracle (oracle/fluxcg.py)."""
+
+    def __init__(self, sizes, M, F, u0, names):
+        self.sizes = list(sizes)
+        self.offsets = np.concatenate([[0], np.cumsum(self.sizes)]).astype(np.int64)
+        self.M = np.asarray(M, dtype=np.float64)
+        self.F = np.asarray(F, dtype=np.float64)
+        self.u0 = np.asarray(u0, dtype=np.float64)
+        self.names = list(names)
+        self._flux = None
+
+    @property
+    def A(self):
+        raise AttributeError("FluxSystem has no assembled A (use .flux)")
+
+
+def assemble_lean(scn) -> FluxSystem:
+    """Fine-grid scenario: M, F, u0 per Eq. app-md / app-mc exactly as assemble_fine
+    builds them (C1, C3, wells), plus flux_form(); no sparse matrix is built."""
+    assert scn["kind"] == "fine"
+    n, h = scn["n"], scn["h"]
+    sizes, Ms, Fs, names = [], [], [], []
+    for cont in scn["continua"]:
+        if cont["kind"] == "grid":
+            N = n * n
+            M = np.full(N, float(cont["c"]) * h * h)                    # C1
+            F = grid_dirichlet_source(n, n, h, cont["k"], cont["dirichlet"])
+            meas = h * h
+        else:
+            N = len(scn["fracture"]["cells"])
+            M = np.full(N, float(cont["c"]) * h)                        # C1
+            F = np.zeros(N)
+            meas = h
+        if "well_q" in cont:
+            F = F + np.asarray(cont["well_q"], dtype=np.float64) * meas * float(cont["well_p"])
+        sizes.append(N)
+        Ms.append(M)
+        Fs.append(F)
+        names.append(cont["name"])
+    u0 = [np.full(s, float(c.get("u0", 0.0))) for s, c in zip(sizes, scn["continua"])]   # C17
+    sys_ = FluxSystem(sizes, np.concatenate(Ms), np.concatenate(Fs), np.concatenate(u0), names)
+    sys_.flux = flux_form(scn, sys_)
+    return sys_
+
+
 def assemble(scn) -> System:
     if scn["kind"] == "fine":
         sys_ = assemble_fine(scn)
@@ -262,9 +324,10 @@ class FluxForm:
         self.between = np.asarray(between, dtype=bool)
         self.diag = np.asarray(diag, dtype=np.float64)
 
-    def block_op(self, sl, mtau, scheme):
-        """Operator of one solve: coupled (whole system, all edges) or the D-scheme
-        block `sl` (A0 block: within-continuum edges, transfer edges as diagonal)."""
+    def block_edges(self, sl, mtau, scheme):
+        """(n, ei, ej, et, d) of one solve: coupled (whole system, all edges) or the
+        D-scheme block `sl` (A0 block: within-continuum edges, transfer edges as
+        diagonal), indices local to the block."""
         lo, hi = sl.start, sl.stop
         if scheme == "coupled":
             keep = np.ones(len(self.ei), dtype=bool)
@@ -275,7 +338,20 @@ class FluxForm:
             for end in (self.ei, self.ej):
                 m = self.between & (end >= lo) & (end < hi)
                 d = d + np.bincount(end[m] - lo, weights=self.et[m], minlength=hi - lo)
-        return BlockOp(hi - lo, self.ei[keep] - lo, self.ej[keep] - lo, self.et[keep], d)
+        return hi - lo, self.ei[keep] - lo, self.ej[keep] - lo, self.et[keep], d
+
+    def block_op(self, sl, mtau, scheme):
+        """Operator of one solve (see block_edges) as a BlockOp."""
+        return BlockOp(*self.block_edges(sl, mtau, scheme))
+
+    def lagged_transfer(self, u):
+        """-A1 u = sum_b Q_ab u_b for every row (the transfer connections only,
+        PAPER.md:482-484): row i of a transfer edge (i, j, sigma) gets sigma u_j, row j
+        gets sigma u_i."""
+        m = self.between
+        ei, ej, et = self.ei[m], self.ej[m], self.et[m]
+        return (np.bincount(ei, weights=et * u[ej], minlength=self.N)
+                + np.bincount(ej, weights=et * u[ei], minlength=self.N))
 
 
 class BlockOp:

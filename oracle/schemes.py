@@ -11,7 +11,8 @@ D-scheme  Eq. si-mc with the D-split:
           i.e. per continuum  (M_a/tau + D_a + sum_b Q_ab) p_a^n
                               = M_a/tau p_a^{n-1} + F_a + sum_b Q_ab p_b^{n-1}.
 F is time-constant (C17).  Solves: SuperLU factorisation once per matrix (tau is
-fixed), one back-solve per step; or the plain Jacobi-PCG of oracle.cg.
+fixed), one back-solve per step (the CG steppers for sizes beyond SuperLU are in
+oracle/fluxcg.py).
 """
 from __future__ import annotations
 
@@ -20,7 +21,6 @@ import scipy.sparse as sp
 import scipy.sparse.linalg as spla
 
 from .assemble import System
-from . import cg as _cg
 
 
 def split_D(sys: System):
@@ -35,35 +35,23 @@ def split_D(sys: System):
 
 
 class _Solver:
-    """x = K^{-1} b for one solve.
-
-    'splu': SuperLU factorisation of the assembled K, then iterative refinement
-            x += K^{-1}(b - K x) with the residual evaluated in long double on the
-            unassembled flux form (FluxForm), until the correction
-            is below 1e-16 ||x||.  The result is the solution of the exact operator,
-            not of its fp64-rounded assembly (reading C15).
-    'cg':   plain Jacobi-PCG (oracle.cg) on the flux-form operator in fp64.
-    """
+    """x = K^{-1} b for one solve: SuperLU factorisation of the assembled K, then
+    iterative refinement x += K^{-1}(b - K x) with the residual evaluated in long
+    double on the unassembled flux form (FluxForm), until the
+    correction is below 1e-16 ||x||.  The result is the solution of the exact operator,
+    not of its fp64-rounded assembly (reading C15).  (Where a factorisation is out of
+    reach, oracle/fluxcg.py steps the same schemes with a plain C Jacobi-PCG.)"""
 
     def __init__(self, op, method="splu", rtol=1e-13, refine=True):
+        if method != "splu":
+            raise ValueError(f"{method}: the CG oracle is oracle.fluxcg")
         self.op = op
-        self.method = method
-        self.rtol = rtol
         self.refine = refine
-        self.iters = []
         self.refinements = []
         self.K = sp.csc_matrix(op.tocsr())
-        if method == "splu":
-            self.lu = spla.splu(self.K)
-        elif method != "cg":
-            raise ValueError(method)
+        self.lu = spla.splu(self.K)
 
     def solve(self, b, x0):
-        if self.method == "cg":
-            x, it = _cg.jacobi_pcg(_FluxMatvec(self.op, self.K.diagonal()), b, x0, rtol=self.rtol,
-                                   maxit=10 * len(b) + 10)
-            self.iters.append(it)
-            return x
         x = self.lu.solve(b)
         k = 0
         if self.refine and np.any(x):
@@ -76,19 +64,6 @@ class _Solver:
                     break
         self.refinements.append(k)
         return x
-
-
-class _FluxMatvec:
-    """K p via the flux form (for the CG oracle); .diagonal() for Jacobi."""
-
-    def __init__(self, op, diag):
-        self.op, self._d = op, diag
-
-    def __matmul__(self, x):
-        return self.op.apply(x)
-
-    def diagonal(self):
-        return self._d
 
 
 class Coupled:

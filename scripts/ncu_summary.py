@@ -24,7 +24,7 @@ for k in ["dram__bytes_read.sum", "dram__bytes_write.sum", "gpu__dram_throughput
           "sm__warps_active.avg.pct_of_peak_sustained_active", "smsp__inst_executed.sum"]:
     val, unit = get(k)
     print(f"{k:60s} {val:>22s} {unit}")
-scale = {"Gbyte": 1e9, "Mbyte": 1e6, "Kbyte": 1e3, "byte": 1.0}
+scale = {"Tbyte": 1e12, "Gbyte": 1e9, "Mbyte": 1e6, "Kbyte": 1e3, "byte": 1.0}
 tsc = {"ms": 1e-3, "us": 1e-6, "ns": 1e-9, "s": 1.0}
 b = sum(float(get(k)[0]) * scale[get(k)[1]] for k in ("dram__bytes_read.sum", "dram__bytes_write.sum"))
 ts = float(get("gpu__time_duration.sum")[0]) * tsc[get("gpu__time_duration.sum")[1]]
