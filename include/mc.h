@@ -158,6 +158,13 @@ typedef struct {
                                                     (NLMC between-continuum entries)        */
 } mc_coupling_desc;
 
+/* Kernel path of a continuum in a step (mc_step_report.paths; informational). */
+enum { MC_PATH_STREAM = 0,            /* grid strips / CSR rows streamed from HBM every iteration   */
+       MC_PATH_ELL_STREAM = 1,        /* fracture network, 64-row ELL chunks streamed               */
+       MC_PATH_ELL_RESIDENT = 2,      /* fracture network resident in shared memory (small network) */
+       MC_PATH_BJ_RESIDENT = 3,       /* block-Jacobi, resident                                     */
+       MC_PATH_BJ_STREAM = 4 };       /* block-Jacobi, two streaming passes                         */
+
 /* Per-step report.  For MC_COUPLED there is one solve (nsolves = 1, index 0). */
 typedef struct {
   int32_t step;                        /* time layer n reached (1-based)                  */
@@ -165,7 +172,8 @@ typedef struct {
   int32_t nsolves;
   int32_t status;                      /* mc_status of the step                            */
   int32_t failed_solve;                /* -1, or the solve index that failed               */
-  int32_t pad;
+  int32_t paths;                       /* kernel path of continuum a in bits 4a..4a+3 (MC_PATH_*): which
+                                          pass streamed its rows, i.e. which byte model applies */
   int64_t iters[MC_MAX_CONTINUA];      /* CG iterations of each solve                      */
   double relres[MC_MAX_CONTINUA];      /* final recursive ||r|| / ||b|| (0 when b = 0)     */
   double bnorm[MC_MAX_CONTINUA];       /* ||b||_2 of each solve                            */
@@ -205,10 +213,20 @@ mc_status mc_step(mc_ctx* ctx, int32_t scheme, mc_step_report* rep);
 mc_status mc_step_decoupled(mc_ctx* ctx, mc_step_report* rep);
 mc_status mc_step_coupled(mc_ctx* ctx, mc_step_report* rep);
 
-/* n_steps steps of `scheme`, enqueued back to back, one synchronisation at the end.
+/* n_steps steps of `scheme` (the time loop of Eq. ct-mc / si-mc).
+ * Coupled, L and U steps, and D steps once the D-scheme's CTA plan is fixed, are enqueued
+ * back to back on mc_options.stream: nothing is read back between them (reports, the
+ * ping-pong index and the failure flag stay on the device) and the host synchronises once
+ * per batch of 256 steps.  The D-scheme's plan (how the CTAs are split between the
+ * concurrent solves) follows the previous step's iteration counts until every solve has
+ * iterated once, at most the first 3 D steps of a context; those planning steps complete
+ * one at a time, exactly as mc_step runs them.  mc_run and a sequence of mc_step calls
+ * therefore give bitwise the same states and iteration counts.
  * reps: NULL or n_steps reports.  snapshots: NULL, or n_steps * n_continua pointers
- * (host or device), snapshots[s * n_continua + a] receives p_a after step s.
- * Stops advancing at the first failed step (later steps are no-ops, reports say so). */
+ * (host or device), snapshots[s * n_continua + a] receives p_a after step s
+ * (stream-ordered copies; contents undefined from the first failed step on).
+ * Stops advancing at the first failed step (later steps are no-ops on the device, their
+ * reports say MC_ERR_STATE); the state is the one before the failed step. */
 mc_status mc_run(mc_ctx* ctx, int32_t scheme, int32_t n_steps, mc_step_report* reps,
                  double* const* snapshots);
 

@@ -44,7 +44,7 @@ def build(force: bool = False, verbose: bool = False, defines=(), out: str | Non
         if r.returncode:
             raise RuntimeError(f"nvcc failed on {src}")
         objs.append(obj)
-    cmd = [NVCC, *ARCH, "-shared", "-o", lib + ".tmp", *objs, "-cudart", "static"]
+    cmd = [NVCC, *ARCH, "-shared", "-o", lib + ".tmp", *objs, "-cudart", "static", "-ldl"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode:
         sys.stderr.write(" ".join(cmd) + "\n" + r.stdout + r.stderr)

@@ -4,6 +4,20 @@
 // derives the operator arrays of Eq. app-mc from the physical
 // inputs in native C++ and uploads them once; every step is one cooperative launch
 // of the sm_100a step kernel (mc_kernels.cu).  Readings C1-C15 of DESIGN.md §3.
+#ifndef MC_NVTX
+#define MC_NVTX 1                          // NVTX ranges `mc_step`, `mc_run` and per-solve marks `pcg[a]`
+#endif
+#if MC_NVTX
+#include <nvtx3/nvToolsExt.h>
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
+#else
+struct NvtxRange {
+  explicit NvtxRange(const char*) {}
+};
+#endif
 #include <algorithm>
 #include <cmath>
 #include <cstdarg>
@@ -22,6 +36,8 @@ using namespace mc;
 namespace {
 
 constexpr int64_t kLargeRows = int64_t(2) << 20;   // "bandwidth-bound" solve
+constexpr int kPlanSteps = 3;                        // D-scheme steps after which the CTA plan is frozen
+constexpr int kRunBatch = 256;                       // mc_run: steps enqueued per synchronisation
 constexpr int64_t kOneCtaWork = 0;                   // rows + stored entries below which a solve gets one CTA
 
 struct HostCont {
@@ -103,6 +119,16 @@ struct mc_ctx {
   int32_t cur_host = 0;
   int32_t step_no = 0;
   int64_t last_iters[MC_MAX_CONTINUA] = {0};
+  // D-scheme CTA plan: re-chosen from the last step's iteration counts until every solve
+  // has a history (at most kPlanSteps steps), then frozen, so that mc_run can enqueue
+  // steps without reading anything back and mc_step follows bitwise the same path
+  int64_t plan_iters[MC_MAX_CONTINUA] = {0};
+  int32_t d_steps = 0;
+  int32_t path_mask = 0;                       // MC_PATH_* per continuum of the last enqueued step
+  bool d_frozen = false;
+  // mc_run: reports and events of one batch of back-to-back steps
+  mc_step_report* rep_run = nullptr;
+  std::vector<cudaEvent_t> run_ev;
   Plan plan[4];                                 // by scheme
   int32_t korder[MC_MAX_CONTINUA] = {0};        // continua by ascending permeability
   bool has_korder = false;
@@ -241,6 +267,7 @@ extern "C" mc_status mc_destroy(mc_ctx* c) {
   for (void* v : c->allocs) cudaFree(v);
   if (c->ev0) cudaEventDestroy(c->ev0);
   if (c->ev1) cudaEventDestroy(c->ev1);
+  for (cudaEvent_t e : c->run_ev) cudaEventDestroy(e);
   delete c;
   return MC_OK;
 }
@@ -1042,7 +1069,7 @@ static Plan make_plan(const mc_ctx* c, int scheme) {
   bool all_large = true, hist = true;
   for (int a = 0; a < L; ++a) {
     if (c->hc[a].n < kLargeRows) all_large = false;
-    if (c->last_iters[a] <= 0) hist = false;
+    if (c->plan_iters[a] <= 0) hist = false;
   }
   int ctas[MC_MAX_CONTINUA] = {0};
   if (all_large || !hist || L == 1 || T < 4 * L) {
@@ -1060,7 +1087,7 @@ static Plan make_plan(const mc_ctx* c, int scheme) {
     double w[MC_MAX_CONTINUA], wsum = 0.0;
     int used = 0;
     for (int a = 0; a < L; ++a) {
-      w[a] = (double)c->hc[a].n * (double)c->last_iters[a];
+      w[a] = (double)c->hc[a].n * (double)c->plan_iters[a];
       wsum += w[a];
       ctas[a] = std::min(useful_ctas(c->hc[a]), std::max(1, T / (2 * L)));
       used += ctas[a];
@@ -1134,7 +1161,8 @@ static bool same_plan(const Plan& a, const Plan& b) {
 }
 
 // ====================================================================== stepping
-static mc_status enqueue_step(mc_ctx* c, int scheme) {
+static mc_status enqueue_step(mc_ctx* c, int scheme, mc_step_report* rep_dev, cudaEvent_t ev0, cudaEvent_t ev1,
+                              int32_t step_no) {
   Plan np = make_plan(c, scheme);
   Plan& cp = c->plan[scheme];
   if (!same_plan(np, cp) || c->uploaded_plan != scheme) {
@@ -1191,6 +1219,13 @@ static mc_status enqueue_step(mc_ctx* c, int scheme) {
         P.cont[a].bjs = (!P.cont[a].bj && nconts == 1 && c->tinv[a] != nullptr && scheme != MC_COUPLED) ? 1 : 0;
       }
   }
+  c->path_mask = 0;
+  for (int a = 0; a < c->L; ++a) {
+    const ContDev& C = P.cont[a];
+    const int path = C.bj ? MC_PATH_BJ_RESIDENT : C.bjs ? MC_PATH_BJ_STREAM : C.resident ? MC_PATH_ELL_RESIDENT
+                     : C.rr ? MC_PATH_ELL_STREAM : MC_PATH_STREAM;
+    c->path_mask |= path << (4 * a);
+  }
   for (int a = 0; a < c->L; ++a) {
     P.cont[a].tinv = c->tinv[a];
     P.cont[a].tcp = c->tcp[a];
@@ -1223,14 +1258,56 @@ static mc_status enqueue_step(mc_ctx* c, int scheme) {
   P.gout = c->gout;
   P.cur = c->cur;
   P.fail = c->fail;
-  P.rep = c->rep;
-  P.step_no = c->step_no + 1;
+  P.rep = rep_dev;
+  P.step_no = step_no;
   P.scheme = scheme;
   CUDA_TRY(c, cudaMemsetAsync(c->sync, 0, sizeof(SyncBlock), c->stream));
-  CUDA_TRY(c, cudaEventRecord(c->ev0, c->stream));
+  CUDA_TRY(c, cudaEventRecord(ev0, c->stream));
   CUDA_TRY(c, launch_step(&P, c->total_ctas, c->stream));
-  CUDA_TRY(c, cudaEventRecord(c->ev1, c->stream));
+  CUDA_TRY(c, cudaEventRecord(ev1, c->stream));
   return MC_OK;
+}
+
+static const char* scheme_name(int scheme) {
+  return scheme == MC_COUPLED ? "coupled" : scheme == MC_DECOUPLED_D ? "D-scheme"
+         : scheme == MC_DECOUPLED_L ? "L-scheme" : "U-scheme";
+}
+
+// host mirrors after a completed step whose report is `rep`
+static mc_status account_step(mc_ctx* c, int scheme, const mc_step_report& rep) {
+#if MC_NVTX
+  for (int g = 0; g < rep.nsolves; ++g) {
+    char buf[96];
+    snprintf(buf, sizeof buf, "pcg[%d] step %d: %lld iterations, %.3f ms", g, rep.step, (long long)rep.iters[g],
+             rep.ms_solve[g]);
+    nvtxMarkA(buf);
+  }
+#endif
+  if (rep.status == MC_OK) {
+    c->cur_host ^= 1;
+    c->step_no += 1;
+    if (scheme == MC_DECOUPLED_D) {
+      for (int a = 0; a < c->L; ++a) c->last_iters[a] = rep.iters[a];
+      if (!c->d_frozen) {
+        // the plan of the next D step is chosen from this step's counts; frozen once every
+        // solve has iterated (or after kPlanSteps steps), DESIGN.md §5.4
+        bool hist = true;
+        for (int a = 0; a < c->L; ++a) {
+          c->plan_iters[a] = rep.iters[a];
+          if (rep.iters[a] <= 0) hist = false;
+        }
+        c->d_steps += 1;
+        if (hist || c->d_steps >= kPlanSteps) c->d_frozen = true;
+      }
+    }
+    return MC_OK;
+  }
+  const char* what = rep.status == MC_ERR_NOCONV ? "no convergence within maxit"
+                     : rep.status == MC_ERR_BREAKDOWN ? "CG breakdown (p.q <= 0)"
+                                                      : "step skipped after an earlier failure";
+  return fail(c, (mc_status)rep.status, "step %d (%s), solve %d: %s after %lld iterations; state not advanced",
+              c->step_no + 1, scheme_name(scheme), rep.failed_solve, what,
+              rep.failed_solve >= 0 ? (long long)rep.iters[rep.failed_solve] : 0LL);
 }
 
 // wait for the step, read its report, update host mirrors
@@ -1241,34 +1318,25 @@ static mc_status complete_step(mc_ctx* c, int scheme, mc_step_report* out) {
   float ms = 0.f;
   CUDA_TRY(c, cudaEventElapsedTime(&ms, c->ev0, c->ev1));
   rep.ms = ms;
-  if (rep.status == MC_OK) {
-    c->cur_host ^= 1;
-    c->step_no += 1;
-    if (scheme == MC_DECOUPLED_D)
-      for (int a = 0; a < c->L; ++a) c->last_iters[a] = rep.iters[a];
-  }
+  rep.paths = c->path_mask;
   if (out) *out = rep;
-  if (rep.status != MC_OK) {
-    const char* what = rep.status == MC_ERR_NOCONV ? "no convergence within maxit"
-                       : rep.status == MC_ERR_BREAKDOWN ? "CG breakdown (p.q <= 0)"
-                                                        : "step skipped after an earlier failure";
-    return fail(c, (mc_status)rep.status, "step %d (%s), solve %d: %s after %lld iterations; state not advanced",
-                c->step_no + 1, scheme == MC_COUPLED ? "coupled" : scheme == MC_DECOUPLED_D ? "D-scheme"
-                : scheme == MC_DECOUPLED_L ? "L-scheme" : "U-scheme", rep.failed_solve, what,
-                rep.failed_solve >= 0 ? (long long)rep.iters[rep.failed_solve] : 0LL);
-  }
-  return MC_OK;
+  return account_step(c, scheme, rep);
 }
 
-static mc_status do_step(mc_ctx* c, int scheme, mc_step_report* rep) {
+static mc_status check_scheme(mc_ctx* c, int scheme) {
   if (!c) return fail(c, MC_ERR_ARG, "NULL context");
   if (scheme < MC_COUPLED || scheme > MC_DECOUPLED_U) return fail(c, MC_ERR_ARG, "unknown scheme %d", scheme);
   if ((scheme == MC_DECOUPLED_L || scheme == MC_DECOUPLED_U) && !c->has_korder)
     return fail(c, MC_ERR_STATE, "L/U scheme before mc_set_permeability_order");
-  mc_status st = finalize(c);
+  return finalize(c);
+}
+
+static mc_status do_step(mc_ctx* c, int scheme, mc_step_report* rep) {
+  mc_status st = check_scheme(c, scheme);
   if (st != MC_OK) return st;
+  NvtxRange range("mc_step");
   CUDA_TRY(c, cudaMemsetAsync(c->fail, 0, 4, c->stream));
-  if ((st = enqueue_step(c, scheme)) != MC_OK) return st;
+  if ((st = enqueue_step(c, scheme, c->rep, c->ev0, c->ev1, c->step_no + 1)) != MC_OK) return st;
   return complete_step(c, scheme, rep);
 }
 
@@ -1309,32 +1377,87 @@ extern "C" mc_status mc_set_permeability_order(mc_ctx* c, const int32_t* order) 
 
 static mc_status copy_out(mc_ctx* c, int a, double* dst);
 
+static void mark_skipped(mc_step_report* reps, int32_t from, int32_t n) {
+  for (int32_t t = from; t < n && reps; ++t) {
+    std::memset(&reps[t], 0, sizeof(mc_step_report));
+    reps[t].status = MC_ERR_STATE;
+    reps[t].failed_solve = -1;
+  }
+}
+
 extern "C" mc_status mc_run(mc_ctx* c, int32_t scheme, int32_t n_steps, mc_step_report* reps,
                             double* const* snapshots) {
-  if (!c) return fail(c, MC_ERR_ARG, "NULL context");
-  if (scheme < MC_COUPLED || scheme > MC_DECOUPLED_U) return fail(c, MC_ERR_ARG, "unknown scheme %d", scheme);
-  if (n_steps < 0) return fail(c, MC_ERR_ARG, "n_steps < 0");
-  mc_status st = finalize(c);
+  mc_status st = check_scheme(c, scheme);
   if (st != MC_OK) return st;
-  for (int32_t s = 0; s < n_steps; ++s) {
+  if (n_steps < 0) return fail(c, MC_ERR_ARG, "n_steps < 0");
+  NvtxRange range("mc_run");
+  auto snap = [&](int32_t s) -> mc_status {
+    if (!snapshots) return MC_OK;
+    for (int a = 0; a < c->L; ++a) {
+      double* dst = snapshots[(size_t)s * c->L + a];
+      mc_status e = dst ? copy_out(c, a, dst) : MC_OK;
+      if (e != MC_OK) return e;
+    }
+    return MC_OK;
+  };
+  int32_t s = 0;
+  // planning steps: while the D-scheme's CTA plan still follows the iteration counts of
+  // the previous step (at most kPlanSteps steps of a context's life) each step is completed
+  // before the next one is planned -- exactly what mc_step does
+  for (; s < n_steps && scheme == MC_DECOUPLED_D && !c->d_frozen; ++s) {
     mc_step_report rep;
     st = do_step(c, scheme, &rep);
     if (reps) reps[s] = rep;
     if (st != MC_OK) {
-      for (int32_t t = s + 1; t < n_steps && reps; ++t) {
-        std::memset(&reps[t], 0, sizeof(mc_step_report));
-        reps[t].status = MC_ERR_STATE;
-        reps[t].failed_solve = -1;
-      }
+      mark_skipped(reps, s + 1, n_steps);
       return st;
     }
-    if (snapshots)
-      for (int a = 0; a < c->L; ++a) {
-        double* dst = snapshots[(size_t)s * c->L + a];
-        if (dst && (st = copy_out(c, a, dst)) != MC_OK) return st;
-      }
+    if ((st = snap(s)) != MC_OK) return st;
   }
-  CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  if (s == n_steps) {
+    CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+    return MC_OK;
+  }
+  // the rest: enqueued back to back (fixed plan, reports and the ping-pong index stay on
+  // the device), one synchronisation per batch of kRunBatch steps
+  if (!c->rep_run && (st = dev_alloc(c, &c->rep_run, (size_t)kRunBatch)) != MC_OK) return st;
+  while ((int)c->run_ev.size() < 2 * kRunBatch) {
+    cudaEvent_t e = nullptr;
+    CUDA_TRY(c, cudaEventCreate(&e));
+    c->run_ev.push_back(e);
+  }
+  std::vector<mc_step_report> hrep((size_t)kRunBatch);
+  CUDA_TRY(c, cudaMemsetAsync(c->fail, 0, 4, c->stream));
+  while (s < n_steps) {
+    const int32_t nb = std::min<int32_t>(kRunBatch, n_steps - s);
+    const int32_t cur0 = c->cur_host;
+    for (int32_t k = 0; k < nb; ++k) {
+      if ((st = enqueue_step(c, scheme, c->rep_run + k, c->run_ev[2 * (size_t)k], c->run_ev[2 * (size_t)k + 1],
+                             c->step_no + 1 + k)) != MC_OK)
+        return st;
+      c->cur_host ^= 1;                       // optimistic mirror for the snapshot copies
+      if ((st = snap(s + k)) != MC_OK) return st;
+    }
+    CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+    CUDA_TRY(c, cudaMemcpy(hrep.data(), c->rep_run, (size_t)nb * sizeof(mc_step_report), cudaMemcpyDeviceToHost));
+    c->cur_host = cur0;
+    for (int32_t k = 0; k < nb; ++k) {
+      float ms = 0.f;
+      CUDA_TRY(c, cudaEventElapsedTime(&ms, c->run_ev[2 * (size_t)k], c->run_ev[2 * (size_t)k + 1]));
+      hrep[(size_t)k].ms = ms;
+      hrep[(size_t)k].paths = c->path_mask;
+      if (reps) reps[s + k] = hrep[(size_t)k];
+      if ((st = account_step(c, scheme, hrep[(size_t)k])) != MC_OK) {
+        // the device skipped every later step of the batch (sticky failure flag)
+        mark_skipped(reps, s + k + 1, n_steps);
+        return st;
+      }
+    }
+    // the last step's events are what mc_last_kernel_ms reports
+    std::swap(c->ev0, c->run_ev[2 * (size_t)(nb - 1)]);
+    std::swap(c->ev1, c->run_ev[2 * (size_t)(nb - 1) + 1]);
+    s += nb;
+  }
   return MC_OK;
 }
 

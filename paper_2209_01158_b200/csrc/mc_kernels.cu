@@ -1871,7 +1871,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) step_kernel(const __grid
       rep->scheme = P.scheme;
       rep->nsolves = P.ngroups;
       rep->failed_solve = -1;
-      rep->pad = 0;
+      rep->paths = 0;
       if (failed) {
         rep->status = MC_ERR_STATE;    // an earlier step of this run failed: skipped
         for (int k = 0; k < MC_MAX_CONTINUA; ++k) {

@@ -57,7 +57,7 @@ class mc_nlmc_desc(C.Structure):
 
 class mc_step_report(C.Structure):
     _fields_ = [("step", _i32), ("scheme", _i32), ("nsolves", _i32), ("status", _i32),
-                ("failed_solve", _i32), ("pad", _i32), ("iters", _i64 * MC_MAX_CONTINUA),
+                ("failed_solve", _i32), ("paths", _i32), ("iters", _i64 * MC_MAX_CONTINUA),
                 ("relres", _d * MC_MAX_CONTINUA), ("bnorm", _d * MC_MAX_CONTINUA),
                 ("ms_solve", _d * MC_MAX_CONTINUA), ("ms", _d)]
 
@@ -65,7 +65,8 @@ class mc_step_report(C.Structure):
         k = self.nsolves
         return dict(step=self.step, scheme=self.scheme, status=self.status, failed_solve=self.failed_solve,
                     iters=list(self.iters[:k]), relres=list(self.relres[:k]), bnorm=list(self.bnorm[:k]),
-                    ms_solve=list(self.ms_solve[:k]), ms=self.ms)
+                    ms_solve=list(self.ms_solve[:k]), ms=self.ms,
+                    paths=[(self.paths >> (4 * a)) & 15 for a in range(MC_MAX_CONTINUA)])
 
 
 EXPORTS = ["mc_create", "mc_set_continuum", "mc_set_coupling", "mc_step_decoupled", "mc_step_coupled",

@@ -1,0 +1,161 @@
+#!/usr/bin/env python
+"""Full-size parity record for the configs no sparse factorisation can take (2 and 4).
+
+    python scripts/parity_full.py --config 4 --scheme D --steps 2 --out profiles/r02_parity_config4_D.json
+
+Both sides run on the SAME box from the same seeded scenario (inputs.make): the CUDA path
+(libmc through the C ABI) steps the GPU, the C Jacobi-PCG oracle (oracle/fluxcg.py, rtol
+1e-13 on the flux form, all host cores; pinned by tests/test_oracle_fluxcg.py) steps its
+own trajectory on the host.  After every step the GPU state is compared per continuum:
+
+    rel L2 = ||u_gpu - u_oracle||_2 / ||u_oracle||_2   (bar: <= 1e-9; exact 0 where the oracle is 0)
+
+This is test infrastructure (the only code here that imports oracle/); the product path
+never does.  Equations: D-scheme PAPER.md:477-486, coupled PAPER.md:374-379.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+CONFIG_RTOL = {0: None, 1: None, 2: None, 3: None, 4: [1e-13, 1e-12]}   # DESIGN.md C25
+
+
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def oracle_only(args):
+    """The oracle's trajectory alone (any host), states saved for a later --load run."""
+    from inputs import make
+    from oracle import assemble as asm, fluxcg
+    scn = make(args.config)
+    tau = scn["T"] / scn["NT"]
+    lean = asm.assemble_lean(scn) if scn["kind"] == "fine" else asm.assemble(scn)
+    st = fluxcg.DSchemeCG(lean, tau) if args.scheme == "D" else fluxcg.CoupledCG(lean, tau)
+    os.makedirs(args.save, exist_ok=True)
+    meta = {"oracle": {"threads": fluxcg.threads(), "os_cpu_count": os.cpu_count(),
+                       "affinity": len(os.sched_getaffinity(0)), "cpu": cpu_model()}, "steps": []}
+    u = lean.u0.copy()
+    for n in range(1, args.steps + 1):
+        t0 = time.perf_counter()
+        u = st.step(u)
+        its = [i[-1] for i in st.iters] if args.scheme == "D" else [st.op.iters[-1]]
+        meta["steps"].append({"step": n, "oracle_s": time.perf_counter() - t0, "oracle_iters": its})
+        np.save(os.path.join(args.save, f"config{args.config}_{args.scheme}_step{n}.npy"), u)
+        json.dump(meta, open(os.path.join(args.save, f"config{args.config}_{args.scheme}.json"), "w"), indent=1)
+        print(json.dumps(meta["steps"][-1]), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--config", type=int, required=True)
+    ap.add_argument("--scheme", default="D", choices=["D", "coupled"])
+    ap.add_argument("--steps", type=int, default=2)
+    ap.add_argument("--precond", default="jacobi", choices=["jacobi", "block"])
+    ap.add_argument("--out", required=True)
+    ap.add_argument("--save", default=None, help="oracle only (no GPU): write its states to DIR/config{c}_{scheme}_step{n}.npy")
+    ap.add_argument("--load", default=None, help="GPU only: compare with oracle states saved by --save (another machine)")
+    args = ap.parse_args()
+    if args.save:
+        return oracle_only(args)
+
+    import torch
+    from inputs import make
+    from oracle import assemble as asm, fluxcg
+    from paper_2209_01158_b200 import Problem, build
+
+    build.build()
+    t0 = time.perf_counter()
+    scn = make(args.config)
+    t_gen = time.perf_counter() - t0
+    tau = scn["T"] / scn["NT"]
+    pb = Problem(scn, rtols=CONFIG_RTOL[args.config], precond=args.precond)
+    t0 = time.perf_counter()
+    lean = asm.assemble_lean(scn) if scn["kind"] == "fine" else asm.assemble(scn)
+    t_asm = time.perf_counter() - t0
+    rec = {"config": args.config, "scheme": args.scheme, "tau": tau, "sizes": lean.sizes,
+           "gpu": {"device": torch.cuda.get_device_name(0), "rtol": CONFIG_RTOL[args.config] or 1e-12,
+                   "precond": args.precond},
+           "oracle": {"kind": "oracle/flux_pcg.c Jacobi-PCG on the flux form", "rtol": 1e-13,
+                      "threads": fluxcg.threads(), "os_cpu_count": os.cpu_count(),
+                      "affinity": len(os.sched_getaffinity(0)), "cpu": cpu_model(),
+                      "assemble_s": t_asm, "generate_s": t_gen},
+           "bar": 1e-9, "steps": []}
+    ok = True
+
+    def flush():
+        rec["pass"] = ok
+        os.makedirs(os.path.dirname(os.path.abspath(args.out)), exist_ok=True)
+        with open(args.out, "w") as f:
+            json.dump(rec, f, indent=1)
+
+    tlast = [time.perf_counter()]
+
+    def check(n, u):
+        nonlocal ok
+        t_or = time.perf_counter() - tlast[0]
+        rep = pb.step(args.scheme)
+        got = [t.cpu().numpy() for t in pb.state()]
+        row = {"step": n, "oracle_s": t_or, "gpu_ms": rep["ms"], "gpu_iters": list(rep["iters"]),
+               "oracle_iters": [op_iters[-1] for op_iters in iters_of()], "rel_l2": [], "oracle_norm": []}
+        for a, ra in enumerate(lean.split(u)):
+            nr = float(np.linalg.norm(ra))
+            if nr == 0.0:
+                e = 0.0 if not got[a].any() else float("inf")
+            else:
+                e = float(np.linalg.norm(got[a] - ra) / nr)
+            row["rel_l2"].append(e)
+            row["oracle_norm"].append(nr)
+            ok = ok and e <= 1e-9
+        rec["steps"].append(row)
+        print(json.dumps(row), flush=True)
+        flush()
+        tlast[0] = time.perf_counter()
+
+    if args.load:
+        meta = json.load(open(os.path.join(args.load, f"config{args.config}_{args.scheme}.json")))
+        rec["oracle"].update(meta["oracle"], where="precomputed on another host by --save, states loaded from disk")
+        its = {r["step"]: r["oracle_iters"] for r in meta["steps"]}
+        secs = {r["step"]: r["oracle_s"] for r in meta["steps"]}
+
+        def iters_of():
+            return [[i] for i in its[len(rec["steps"]) + 1]]
+
+        for n in range(1, args.steps + 1):
+            u = np.load(os.path.join(args.load, f"config{args.config}_{args.scheme}_step{n}.npy"))
+            tlast[0] = time.perf_counter() - secs[n]
+            check(n, u)
+    else:
+        st = fluxcg.DSchemeCG(lean, tau) if args.scheme == "D" else fluxcg.CoupledCG(lean, tau)
+
+        def iters_of():
+            return st.iters if args.scheme == "D" else [st.op.iters]
+
+        u = lean.u0.copy()
+        tlast[0] = time.perf_counter()
+        for n in range(1, args.steps + 1):
+            u = st.step(u)                       # the oracle's own trajectory
+            check(n, u)
+    flush()
+    pb.close()
+    print("PASS" if ok else "FAIL", args.out)
+    sys.exit(0 if ok else 1)
+
+
+if __name__ == "__main__":
+    main()
