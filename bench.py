@@ -7,9 +7,11 @@
 One "step" is one time layer of the D-scheme over the whole
 workload: the lagged right-hand side of every continuum, one Jacobi-PCG solve per
 continuum to rtol 1e-12 and the commit — one launch of libmc's persistent step
-kernel.  Default workload: BASELINE.json configs[1] (1024^2 matrix + 72,738
-fracture cells, log-normal k).  The inputs are seeded synthetic
-(inputs/); nothing here reads /root/reference.
+kernel.  Default workload: BASELINE.json configs[4], the largest single-GPU fine-grid
+configuration (8192^2 matrix + 16,615,213 fracture cells, log-normal k, 83.7M DOF;
+DESIGN.md §7) -- the one BASELINE.json's HBM target is stated on; `--config 1` is the
+1024^2 case (L2-resident, latency-bound).  The inputs are seeded synthetic (inputs/);
+nothing here reads /root/reference.
 
 Timing: W untimed warm-up steps, then exactly K steps, each bracketed by CUDA
 events on the stream libmc launches on; L2 is flushed (256 MiB memset) between
@@ -43,7 +45,7 @@ def parse():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", type=int, default=1)
+    ap.add_argument("--config", type=int, default=4)
     ap.add_argument("--scheme", default="D", choices=["D", "coupled", "L", "U"])
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -62,14 +64,18 @@ def peaks():
     return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)"
 
 
-def ncu_traffic(cid, warmup):
+def ncu_traffic(cid, precond):
     """Mean DRAM bytes (read + write) per step_kernel launch from the committed ncu launch
-    list of this bench command (profiles/r01_launches_config{cid}.csv), warm-up launches
-    skipped; None when no such capture is committed."""
+    list of this bench command (profiles/rNN_launches_config{cid}[_block].csv, newest round
+    first; the timed launches = the last `timed` rows of the list named in its .json
+    sidecar, else all but the first 3); None when no such capture is committed."""
     import csv
-    p = os.path.join(ROOT, "profiles", f"r01_launches_config{cid}.csv")
-    if not os.path.exists(p):
+    import glob
+    suf = "_block" if precond == "block" else ""
+    cands = sorted(glob.glob(os.path.join(ROOT, "profiles", f"r*_launches_config{cid}{suf}.csv")), reverse=True)
+    if not cands:
         return None, None
+    p = cands[0]
     rows = [r for r in csv.reader(l for l in open(p) if not l.startswith("=="))]
     hdr = rows[0]
     ik, im, iv = hdr.index("Kernel Name"), hdr.index("Metric Name"), hdr.index("Metric Value")
@@ -78,7 +84,11 @@ def ncu_traffic(cid, warmup):
         if "step_kernel" in r[ik] and r[im] in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
             per.setdefault(r[0], 0.0)
             per[r[0]] += float(r[iv].replace(",", ""))
-    vals = [per[k] for k in sorted(per, key=int)][warmup:]
+    skip = 3
+    side = p[:-4] + ".json"
+    if os.path.exists(side):
+        skip = int(json.load(open(side)).get("warmup_launches", 3))
+    vals = [per[k] for k in sorted(per, key=int)][skip:]
     if not vals:
         return None, None
     return sum(vals) / len(vals), os.path.relpath(p, ROOT)
@@ -91,24 +101,35 @@ def workload_name(cid, scheme):
 
 
 # ------------------------------------------------------------------ algorithmic bytes
-def step_bytes(pb, rep, scheme, precond="jacobi"):
-    """Algorithmic HBM bytes of one step kernel: per CG iteration every
-    row reads x, r, q, p, D^-1 and its shift, writes x, r, p, q once; grid rows read
-    Tx, Ty; graph rows read their row pointer and column indices (values when not
-    uniform).  Init pass: ~76 B/row + 16 B per transfer entry.  Neighbour gathers are
-    cache hits and not counted.  Block-Jacobi networks (precond "block", §5.2c) make two
-    passes per iteration: U reads r, q, p, x and two Thomas factors (1/pivot, e; c' is
-    recomputed), writes x, r, z (72 B); S reads z, p_old, shift and 16 B of codes, writes p, q (56 B)."""
+PATH_NAMES = {0: "stream", 1: "ell-stream", 2: "ell-resident", 3: "bj-resident", 4: "bj-stream"}
+
+
+def row_bytes(kind, path, nnz_off):
+    """Algorithmic HBM bytes per row and CG iteration of the pass that handles a continuum
+    (DESIGN.md §5.3 / §6; mc_step_report.paths says which pass ran):
+      grid strips          read x, r, q, p, D^-1, Tx, Ty, shift (64) + write x, r, p, q (32) = 96
+      streamed ELL chunks  read x, r, q, p, D^-1, shift (48) + 4 int32 codes (16) + write 32 = 96
+      CSR rows             read 48 + row pointer 4 + 4 (col) or 12 (col + T) per entry + write 32
+      resident ELL         the network's state stays in shared memory: only r, p, q are
+                           published for the other warps' gathers (24)
+      block-Jacobi         resident: z, p published (16); streaming two-pass: 72 + 56 = 128
+    Neighbour gathers are cache hits and are not counted."""
+    if kind == "grid":
+        return 96.0
+    return {0: 84.0 + nnz_off, 1: 96.0, 2: 24.0, 3: 16.0, 4: 128.0}[path]
+
+
+def step_bytes(pb, rep, scheme):
+    """Algorithmic HBM bytes of one step kernel: iterations x rows x row_bytes per continuum,
+    plus the init pass (~76 B/row)."""
     sizes, kinds, nnz_off = pb.byte_model
-    total = 0.0
-    iters = rep["iters"]
+    total, per_cont = 0.0, []
     for a, n in enumerate(sizes):
-        per = 96.0 if kinds[a] == "grid" else 84.0 + nnz_off[a]
-        if precond == "block" and kinds[a] != "grid" and scheme != "coupled":
-            per = 128.0
-        it = iters[0] if scheme == "coupled" else iters[a]
-        total += it * per * n + 76.0 * n
-    return total
+        it = rep["iters"][0] if scheme == "coupled" else rep["iters"][a]
+        b = it * row_bytes(kinds[a], rep["paths"][a], nnz_off[a]) * n + 76.0 * n
+        per_cont.append(b)
+        total += b
+    return total, per_cont
 
 
 def model_for(scn):
@@ -217,10 +238,29 @@ def aggregate(world, dof, steps, total_ms):
 
 
 # ------------------------------------------------------------------ oracle legs (CPU)
+# Oracle Jacobi-PCG iterations per step and continuum (rtol 1e-13, D-scheme, step 2 of the
+# oracle's own trajectory) for the configs whose full oracle step takes minutes to an hour:
+# measured by scripts/parity_full.py (profiles/r02_parity_config{2,4}_D.json).  Used only to
+# scale a bounded sample of oracle iterations to one whole step.
+ORACLE_ITERS = {2: [480, 430, 28000], 4: [400, 57000]}   # PLACEHOLDER until the parity records exist
+
+
+def host_info():
+    model = "unknown"
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    return {"os_cpu_count": os.cpu_count(), "affinity": len(os.sched_getaffinity(0)), "cpu_model": model}
+
+
 def oracle_sample(scn, scheme, steps, budget_s=30.0, warmup=0):
-    """Time the CPU oracle (as it stands) on `steps` steps of the workload after `warmup`
-    untimed ones; setup (assembly + SuperLU factorisation) excluded and reported
-    separately."""
+    """Configs 0, 1, 3: time the SuperLU oracle (as it stands, one thread) on `steps` whole
+    steps of the workload after `warmup` untimed ones; setup (assembly + factorisation)
+    excluded and reported separately.  Returns (dof, steps done, seconds, setup seconds)."""
     os.environ.setdefault("OMP_NUM_THREADS", "1")
     from oracle import assemble as asm, schemes
     t0 = time.perf_counter()
@@ -242,24 +282,106 @@ def oracle_sample(scn, scheme, steps, budget_s=30.0, warmup=0):
     return sum(sys_.sizes), done, el, setup
 
 
+class CgOracleSampler:
+    """Configs 2 and 4 (no factorisation fits): the C Jacobi-PCG oracle
+    (oracle/flux_pcg.c, OpenMP on all host cores) as it stands.  One whole oracle step takes
+    minutes (config 2) to an hour (config 4), so a sample is a bounded number of PCG
+    iterations of every continuum's D-scheme system from a seeded state; the per-iteration
+    times are scaled by the iterations a whole step needs (`iters_per_step`)."""
+
+    def __init__(self, scn, sample_iters):
+        import numpy as np
+        from oracle import assemble as asm, fluxcg
+        self.fluxcg = fluxcg
+        t0 = time.perf_counter()
+        self.lean = asm.assemble_lean(scn)
+        self.st = fluxcg.DSchemeCG(self.lean, scn["T"] / scn["NT"])
+        self.setup = time.perf_counter() - t0
+        u = np.random.default_rng(0).random(len(self.lean.M))         # a previous layer in (0, 1)
+        self.u, self.b = u, self.st.rhs(u)
+        self.sample_iters = list(sample_iters)
+        self.threads = fluxcg.threads()
+
+    def sample(self):
+        """Seconds per PCG iteration of every continuum (one capped solve each)."""
+        out = []
+        for a, k in enumerate(self.sample_iters):
+            s = self.lean.block(a)
+            t0 = time.perf_counter()
+            try:
+                self.st.ops[a].solve(self.b[s], self.u[s], 1e-13, maxit=k)
+                k = self.st.ops[a].iters[-1]                          # converged early (small system)
+            except self.fluxcg.CGNoConvergence:
+                pass
+            out.append((time.perf_counter() - t0) / max(k, 1))
+        return out
+
+
+def cg_sample_iters(cid):
+    return {2: [20, 20, 200], 4: [20, 100]}[cid]    # ~5-10 s of host work per sample (16 cores)
+
+
 def run_reference(args):
     rank, world, _ = dist_init(args.gpus)
     if rank != 0:
         return
     from inputs import make
     scn = make(args.config)
-    dof, done, el, setup = oracle_sample(scn, args.scheme, args.steps, budget_s=240.0, warmup=args.warmup)
-    value = dof * done / el
-    line = {"metric": "fine-grid DOF-steps/s (decoupled, fp64)", "value": value, "unit": "DOF-steps/s",
-            "n_gpus": args.gpus, "steps": done, "warmup": args.warmup, "ms_per_step": 1e3 * el / done,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic", "impl": "reference",
-            "config": {"workload": workload_name(args.config, args.scheme), "dof": dof, "scheme": args.scheme},
-            "cpu_baseline": {"value": value, "unit": "DOF-steps/s", "cores": 1, "kind": "oracle",
-                             "sample": f"{done} full oracle steps (SuperLU back-solves + long-double "
-                                       f"flux-form refinement, 1 thread); setup {setup:.1f}s excluded"},
-            "e2e": {"value": value, "unit": "DOF-steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    base = {"metric": "fine-grid DOF-steps/s (decoupled, fp64)", "unit": "DOF-steps/s", "n_gpus": args.gpus,
+            "warmup": args.warmup, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f64", "data": "synthetic", "impl": "reference"}
+    if args.config in (2, 4) and args.scheme == "D":
+        smp = CgOracleSampler(scn, cg_sample_iters(args.config))
+        dof = sum(smp.lean.sizes)
+        need = ORACLE_ITERS[args.config]
+        for _ in range(args.warmup):
+            smp.sample()
+        secs = []
+        for _ in range(args.steps):
+            per = smp.sample()
+            secs.append(sum(t * n for t, n in zip(per, need)))
+        el = sum(secs)
+        value = dof * args.steps / el
+        sample = (f"each step = {smp.sample_iters} Jacobi-PCG iterations per continuum of the C oracle "
+                  f"(oracle/flux_pcg.c, {smp.threads} OpenMP threads) on config {args.config}'s D-scheme systems "
+                  f"from a seeded state, scaled to the {need} iterations per continuum a whole oracle step "
+                  f"needs (profiles/r02_parity_config{args.config}_D.json); setup {smp.setup:.0f}s excluded")
+        line = dict(base, value=value, steps=args.steps, ms_per_step=1e3 * el / args.steps,
+                    config={"workload": workload_name(args.config, args.scheme), "dof": dof, "scheme": args.scheme},
+                    cpu_baseline={"value": value, "unit": "DOF-steps/s", "cores": smp.threads, "kind": "oracle",
+                                  "sample": sample, "host": host_info()})
+    else:
+        dof, done, el, setup = oracle_sample(scn, args.scheme, args.steps, budget_s=240.0, warmup=args.warmup)
+        value = dof * done / el
+        line = dict(base, value=value, steps=done, ms_per_step=1e3 * el / done,
+                    config={"workload": workload_name(args.config, args.scheme), "dof": dof, "scheme": args.scheme},
+                    cpu_baseline={"value": value, "unit": "DOF-steps/s", "cores": 1, "kind": "oracle",
+                                  "sample": f"{done} full oracle steps (SuperLU back-solves + long-double "
+                                            f"flux-form refinement, 1 thread); setup {setup:.1f}s excluded",
+                                  "host": host_info()})
+    line["e2e"] = {"value": line["value"], "unit": "DOF-steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}
     print(json.dumps(line), flush=True)
+
+
+def cpu_baseline_leg(args, scn, reps):
+    """The oracle timed on this box's host cores on a bounded sample of the workload."""
+    if args.config in (2, 4) and args.scheme == "D":
+        smp = CgOracleSampler(scn, cg_sample_iters(args.config))
+        per = smp.sample()
+        need = [sum(r["iters"][a] for r in reps) / len(reps) for a in range(len(per))]
+        sec = sum(t * n for t, n in zip(per, need))
+        dof = sum(smp.lean.sizes)
+        return {"value": dof / sec, "unit": "DOF-steps/s", "cores": smp.threads, "kind": "oracle",
+                "sample": (f"config{args.config} D-scheme: {smp.sample_iters} Jacobi-PCG iterations per continuum of "
+                           f"the C oracle (oracle/flux_pcg.c, {smp.threads} OpenMP threads) from a seeded state = "
+                           f"{['%.4f' % t for t in per]} s per iteration, scaled to the timed steps' mean "
+                           f"iteration counts {[round(n, 1) for n in need]}; setup {smp.setup:.0f}s excluded"),
+                "host": host_info()}
+    d, done, el, setup = oracle_sample(scn, args.scheme, 3 if args.config == 1 else 20, budget_s=25.0)
+    return {"value": d * done / el, "unit": "DOF-steps/s", "cores": 1, "kind": "oracle",
+            "sample": f"config{args.config} {args.scheme}-scheme, {done} oracle steps (SuperLU back-solves "
+                      f"+ long-double flux refinement, 1 thread); assembly+factorisation {setup:.1f}s excluded",
+            "host": host_info()}
 
 
 # ------------------------------------------------------------------ main
@@ -283,6 +405,7 @@ def main():
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
     for _ in range(args.warmup):
         pb.step(args.scheme)
+    saved = [t.clone() for t in pb.state()]          # the e2e leg replays the same K steps from here
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     reps = []
     clocks = Clocks(local)
@@ -301,43 +424,55 @@ def main():
     total_ms = max_over_ranks(sum(step_ms), world)
     value = aggregate(world, dof, args.steps, total_ms)
     # roofline of the dominant (only) kernel: the step kernel, one launch per step
-    bytes_per = sum(step_bytes(pb, r, args.scheme, args.precond) for r in reps) / args.steps
+    sb = [step_bytes(pb, r, args.scheme) for r in reps]
+    bytes_per = sum(b for b, _ in sb) / args.steps
     kern_ms = sum(r["ms"] for r in reps) / args.steps
     peak, peak_src = peaks()
     achieved = bytes_per / (kern_ms * 1e-3) / 1e9
-    traffic, traffic_src = (ncu_traffic(args.config, 3) if args.scheme == "D" and args.precond == "jacobi"
-                            else (None, None))
-    # end to end through the C ABI with host buffers (pinned), copies inside the timed region
+    traffic, traffic_src = (ncu_traffic(args.config, args.precond) if args.scheme == "D" else (None, None))
+    nsol = len(reps[0]["iters"])
+    mean_its = [sum(r["iters"][a] for r in reps) / len(reps) for a in range(nsol)]
+    mean_ms = [sum(r["ms_solve"][a] for r in reps) / len(reps) for a in range(nsol)]
+    per_solve = []
+    if args.scheme != "coupled":
+        for a in range(nsol):
+            ba = sum(pc[a] for _, pc in sb) / args.steps
+            per_solve.append({"rows": pb.sizes[a], "path": PATH_NAMES[reps[-1]["paths"][a]],
+                              "us_per_iteration": 1e3 * mean_ms[a] / max(mean_its[a], 1.0),
+                              "GBps": ba / max(mean_ms[a], 1e-9) / 1e6})
+    # end to end through the C ABI with host buffers (pinned): the SAME K steps replayed from
+    # the saved state with the same L2 policy; every step's state goes host -> device before
+    # the step and device -> host after it, copies inside the timed region
     e2e = None
     if not args.no_e2e:
         host = [torch.empty(s, dtype=torch.float64, pin_memory=True) for s in pb.sizes]
         for a in range(pb.L):
-            pb.get_state(a, out=host[a])
+            host[a].copy_(saved[a])
         torch.cuda.synchronize()
         barrier(world)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
+        ereps = []
         for _ in range(args.steps):
+            flush.zero_()
             for a in range(pb.L):
                 pb.set_state(a, host[a])
-            pb.step(args.scheme)
+            ereps.append(pb.step(args.scheme))
             for a in range(pb.L):
                 pb.get_state(a, out=host[a])
         e1.record(stream)
         torch.cuda.synchronize()
         e2e_ms = max_over_ranks(e0.elapsed_time(e1), world)
         e2e = {"value": world * dof * args.steps / (e2e_ms * 1e-3), "unit": "DOF-steps/s",
-               "h2d_bytes_per_step": 8 * dof, "d2h_bytes_per_step": 8 * dof}
+               "h2d_bytes_per_step": 8 * dof, "d2h_bytes_per_step": 8 * dof,
+               "same_steps_as_value": [r["iters"] for r in ereps] == [r["iters"] for r in reps],
+               "region": "K x (L2 flush + mc_set_state from pinned host + mc_step + mc_get_state to pinned host)"}
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        d, done, el, setup = oracle_sample(scn, args.scheme, 3 if args.config in (1, 2, 4) else 20, budget_s=25.0)
-        cpu = {"value": d * done / el, "unit": "DOF-steps/s", "cores": 1, "kind": "oracle",
-               "sample": f"config{args.config} {args.scheme}-scheme, {done} oracle steps (SuperLU back-solves "
-                         f"+ long-double flux refinement, 1 thread); assembly+factorisation {setup:.1f}s excluded"}
-    its = [r["iters"] for r in reps]
-    # metric name follows the scheme actually timed
-    mean_its = [sum(x[a] for x in its) / len(its) for a in range(len(its[0]))]
+        cpu = cpu_baseline_leg(args, scn, reps)
     if rank == 0:
+        l2res = all(p["path"] in ("ell-resident", "bj-resident") or p["rows"] * 96 < 100e6 for p in per_solve) \
+            if per_solve else False
         line = {
             "metric": "fine-grid DOF-steps/s (decoupled, fp64)" if args.scheme == "D" else
                       f"fine-grid DOF-steps/s ({args.scheme}-scheme, fp64)", "value": value, "unit": "DOF-steps/s",
@@ -347,15 +482,19 @@ def main():
             "config": {"workload": workload_name(args.config, args.scheme), "dof": dof,
                        "sizes": pb.sizes, "scheme": args.scheme, "rtol": CONFIG_RTOL[args.config] or 1e-12,
                        "precond": args.precond,
-                       "cg_iters_per_step": mean_its,
-                       "ms_per_solve": [sum(r["ms_solve"][a] for r in reps) / len(reps) for a in range(len(reps[0]["ms_solve"]))],
+                       "time_layers": f"{args.warmup + 1}..{args.warmup + args.steps} of the run from u0 "
+                                      f"(the config's own N_T is {scn['NT']})",
+                       "cg_iters_per_step": mean_its, "ms_per_solve": mean_ms,
                        "l2": "flushed between timed steps (256 MiB memset)",
                        "parallelism": f"replicas x{world}"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "traffic_source": traffic_src,
-                         "peak_source": peak_src,
+                         "peak_source": peak_src, "frac_of_8TBps": achieved / 8000.0,
                          "kernel": "mc::step_kernel", "bytes_per_launch": bytes_per,
-                         "ms_per_launch": kern_ms},
+                         "ms_per_launch": kern_ms, "per_solve": per_solve,
+                         "regime": ("working set L2-resident: latency-bound, frac is not an HBM fraction "
+                                    "(see per_solve us_per_iteration; barrier floor profiles/r01_barrier.txt)"
+                                    if l2res else "working set >> L2: HBM-bound")},
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": args.steps, "clocks": clk,
         }
         print(json.dumps(line), flush=True)
