@@ -102,6 +102,7 @@ struct mc_ctx {
   double* val[MC_MAX_CONTINUA] = {nullptr};
   int32_t* ecol[MC_MAX_CONTINUA] = {nullptr};
   int32_t* perm[MC_MAX_CONTINUA] = {nullptr};   // graph: internal -> caller numbering
+  double* rec[MC_MAX_CONTINUA][2] = {{nullptr, nullptr}};   // streaming ELL pass: {r, q, p, D^-1} records
   double* tinv[MC_MAX_CONTINUA] = {nullptr};    // bj: chunk Thomas factors
   double* tcp[MC_MAX_CONTINUA] = {nullptr};
   double* tem[MC_MAX_CONTINUA] = {nullptr};
@@ -1010,6 +1011,15 @@ static int64_t one_cta_work() {
   return w;
 }
 
+// MC_RECORDS=0 (dev): keep the streaming ELL pass on the separate r, q, p arrays
+static bool use_records() {
+  static const bool v = [] {
+    const char* e = getenv("MC_RECORDS");
+    return !(e && e[0] == '0');
+  }();
+  return v;
+}
+
 static int useful_ctas(const HostCont& H) {
   const int64_t work = H.kind == KIND_GRID ? 5 * H.n : H.n + H.col_count;
   if (work <= one_cta_work()) return 1;
@@ -1217,6 +1227,20 @@ static mc_status enqueue_step(mc_ctx* c, int scheme, mc_step_report* rep_dev, cu
         P.cont[a].bj = (nconts == 1 && nch <= (int64_t)G.cta_count * kWarps && c->tinv[a] != nullptr &&
                         scheme != MC_COUPLED) ? 1 : 0;
         P.cont[a].bjs = (!P.cont[a].bj && nconts == 1 && c->tinv[a] != nullptr && scheme != MC_COUPLED) ? 1 : 0;
+        // streaming Jacobi pass of a decoupled solve: CG state as 32-byte records (allocated
+        // the first time a plan streams this network)
+        if (use_records() && nconts == 1 && scheme != MC_COUPLED && !P.cont[a].resident && !P.cont[a].bj && !P.cont[a].bjs) {
+          if (!c->rec[a][0]) {
+            const size_t cnt = (size_t)4 * ((size_t)c->hc[a].n + 64 + kSlack);
+            for (int k = 0; k < 2; ++k) {
+              mc_status st = dev_alloc(c, &c->rec[a][k], cnt);
+              if (st != MC_OK) return st;
+              CUDA_TRY(c, cudaMemsetAsync(c->rec[a][k], 0, cnt * 8, c->stream));
+            }
+          }
+          P.cont[a].rec[0] = c->rec[a][0];
+          P.cont[a].rec[1] = c->rec[a][1];
+        }
       }
   }
   c->path_mask = 0;

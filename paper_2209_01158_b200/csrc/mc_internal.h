@@ -64,6 +64,8 @@ struct ContDev {
   int32_t resident;        // rr + every warp owns <= kStages chunks: state stays in shared memory
   int32_t bj;              // resident, one chunk per warp, block-Jacobi preconditioner (§8(f) rank 4)
   int32_t bjs;             // block-Jacobi, streaming passes (network too large to stay resident)
+  double* rec[2];          // streaming ELL pass (Jacobi, D-scheme): CG state as 32-byte records
+                           // {r, q, p, D^-1} per row, double-buffered by iteration parity
   const double* tinv;      // bj: Thomas factors of each 64-row chunk's tridiagonal block:
   const double* tcp;       //     1 / pivot, super-diagonal multiplier c', sub-diagonal e_{i-1}
   const double* tem;

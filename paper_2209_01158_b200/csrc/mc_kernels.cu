@@ -62,6 +62,19 @@ __device__ __forceinline__ double pnew(double ro, double qo, double po, double d
   return __fma_rn(di, rn, __dmul_rn(b, po));
 }
 
+// 32-byte CG-state records {r, q, p, D^-1} of the streaming ELL pass: one 256-bit access each
+__device__ __forceinline__ void st_rec(double* rec, double r, double q, double p, double d) {
+  asm volatile("st.global.cg.v4.f64 [%0], {%1,%2,%3,%4};" ::"l"(rec), "d"(r), "d"(q), "d"(p), "d"(d) : "memory");
+}
+struct Rec4 {
+  double r, q, p, d;
+};
+__device__ __forceinline__ Rec4 ld_rec(const double* rec) {
+  Rec4 v;
+  asm volatile("ld.global.cg.v4.f64 {%0,%1,%2,%3}, [%4];" : "=d"(v.r), "=d"(v.q), "=d"(v.p), "=d"(v.d) : "l"(rec) : "memory");
+  return v;
+}
+
 #if MC_PROF
 // dev instrumentation (-DMC_PROF=1 builds only): clock64 per phase of the CG loop,
 // summed over iterations by thread 0 of each group's first CTA
@@ -681,6 +694,149 @@ __device__ void iter_ells(const Ctx& c, const ContDev& C, int wg, int W, const S
   }
 }
 
+// Streaming ELL pass on 32-byte records (Jacobi, D-scheme).  Same sweep
+// and arithmetic as iter_ells, but the CG state of the network lives in records
+// {r, q, p, D^-1} per row (C.rec[s], double-buffered by iteration parity):
+//   * the chunk window (64 rows + 2-row halos) arrives with ONE bulk copy of 2 176 B;
+//   * a far neighbour costs ONE 256-bit load of one 32-byte sector instead of four 8-byte
+//     loads from four arrays (four sectors) -- the far gathers of the vertical segments
+//     were the pass's L2 -> SM traffic (128 of 192 B per row);
+//   * the new record leaves with one 256-bit store per row.
+// Lane l owns rows l and l + 32 of the chunk (records 32 B apart: 2-way bank conflicts on
+// the 128-bit shared loads instead of 4-way with rows 2l, 2l + 1).
+struct FarR {
+  double w0, w1, w2, w3;
+  int s0, s1, s2, s3;
+};
+
+__device__ __forceinline__ void ell_codes_r(const double* sl, int lane, int32_t (&j)[2][4]) {
+  const int32_t* si = reinterpret_cast<const int32_t*>(sl + 400);
+#pragma unroll
+  for (int h = 0; h < 2; ++h)
+#pragma unroll
+    for (int k = 0; k < 4; ++k) j[h][k] = si[k * 64 + lane + 32 * h];
+}
+
+__device__ __forceinline__ double pn_rec(const Rec4& v, double a, double b) { return pnew(v.r, v.q, v.p, v.d, a, b); }
+
+__device__ void iter_ells4(const Ctx& c, const ContDev& C, int wg, int W, const Stage& st, int s,
+                           double (&acc)[kNPart]) {
+  double* wsm = st.wsm;
+  double* pnb = wsm + kWarpSmem - kPnBuf;                      // new p of the window rows
+  const int lane = threadIdx.x & 31;
+  const int64_t off = C.off, es = C.estride;
+  const int r1 = (int)C.n;
+  const int nch = (r1 + 63) / 64;
+  const double* recs = C.rec[s];
+  double* recd = C.rec[s ^ 1];
+  auto tix = [&](int m) { return (m / W) % kStagesE; };
+  auto prefetch = [&](int m) {
+    const int t = tix(m);
+    double* sl = wsm + t * kSlotE;
+    __syncwarp();
+    if (lane == 0) {
+      const int64_t b = 64 * (int64_t)m;
+      const bool full = b >= 2;                                 // window start in bounds
+      const unsigned wb = full ? 68u * 32u : 66u * 32u;
+      st.begin(t, wb + 2u * 512u + 4u * 256u);
+      uint64_t* bar = st.bars + t;
+      bulk_g2s(sl + (full ? 0 : 8), recs + 4 * (b - (full ? 2 : 0)), wb, bar);
+      bulk_g2s(sl + 272, c.x + off + b, 512, bar);
+      bulk_g2s(sl + 336, c.ds + off + b, 512, bar);
+      int32_t* si = reinterpret_cast<int32_t*>(sl + 400);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) bulk_g2s(si + k * 64, C.ecol + k * es + b, 256, bar);
+    }
+  };
+  if (wg >= nch) return;
+  prefetch(wg);
+  for (int m = wg; m < nch; m += W) {
+    if (m + W < nch) prefetch(m + W);                             // next chunk in flight
+    st.wait(tix(m));
+    const double* sl = wsm + tix(m) * kSlotE;
+    int32_t j[2][4];
+    ell_codes_r(sl, lane, j);
+    // far neighbours of this lane's two rows: up to 4 records gathered in one batch
+    FarR f;
+    f.s0 = f.s1 = f.s2 = f.s3 = -1;
+    int32_t i0 = -1, i1 = -1, i2 = -1, i3 = -1;
+    {
+      int nfar = 0;
+#pragma unroll
+      for (int h = 0; h < 2; ++h)
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+          if (j[h][k] >= 0) {
+            if (nfar == 0) {
+              i0 = j[h][k];
+              f.s0 = 4 * h + k;
+            } else if (nfar == 1) {
+              i1 = j[h][k];
+              f.s1 = 4 * h + k;
+            } else if (nfar == 2) {
+              i2 = j[h][k];
+              f.s2 = 4 * h + k;
+            } else if (nfar == 3) {
+              i3 = j[h][k];
+              f.s3 = 4 * h + k;
+            }
+            ++nfar;
+          }
+    }
+    f.w0 = f.w1 = f.w2 = f.w3 = 0.0;
+    if (i0 >= 0) f.w0 = pn_rec(ld_rec(recs + 4 * ((int64_t)i0 - off)), c.a, c.b);
+    if (i1 >= 0) f.w1 = pn_rec(ld_rec(recs + 4 * ((int64_t)i1 - off)), c.a, c.b);
+    if (i2 >= 0) f.w2 = pn_rec(ld_rec(recs + 4 * ((int64_t)i2 - off)), c.a, c.b);
+    if (i3 >= 0) f.w3 = pn_rec(ld_rec(recs + 4 * ((int64_t)i3 - off)), c.a, c.b);
+    const int base = 64 * m;
+    double pc[2], rc[2], dc[2], po[2];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int w = 2 + lane + 32 * h;
+      const double2 rq = *reinterpret_cast<const double2*>(sl + 4 * w);
+      const double2 pd = *reinterpret_cast<const double2*>(sl + 4 * w + 2);
+      rc[h] = __fma_rn(-c.a, rq.y, rq.x);
+      dc[h] = pd.y;
+      po[h] = pd.x;
+      pc[h] = __fma_rn(dc[h], rc[h], __dmul_rn(c.b, po[h]));
+    }
+    __syncwarp();                                                 // previous chunk's pnb reads done
+    pnb[2 + lane] = pc[0];
+    pnb[34 + lane] = pc[1];
+    if (lane < 4) {                                               // halo rows 0, 1, 66, 67
+      const int w = lane < 2 ? lane : 64 + lane;
+      pnb[w] = pnew(sl[4 * w], sl[4 * w + 1], sl[4 * w + 2], sl[4 * w + 3], c.a, c.b);
+    }
+    __syncwarp();
+    double qv[2];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      double sum = 0.0;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const int32_t cd = j[h][k];
+        double v = pc[h];                                          // -1: no neighbour
+        if (cd <= -2) v = pnb[-2 - cd];
+        else if (cd >= 0) {
+          if (f.s0 == 4 * h + k) v = f.w0;
+          else if (f.s1 == 4 * h + k) v = f.w1;
+          else if (f.s2 == 4 * h + k) v = f.w2;
+          else if (f.s3 == 4 * h + k) v = f.w3;
+          else v = pn_rec(ld_rec(recs + 4 * ((int64_t)cd - off)), c.a, c.b);   // rare: > 4 far in this lane
+        }
+        sum += pc[h] - v;
+      }
+      const int row = base + lane + 32 * h;
+      qv[h] = sl[336 + lane + 32 * h] * pc[h] + C.Tconst * sum;
+      if (row < r1) {
+        c.x[off + row] = __fma_rn(c.a, po[h], sl[272 + lane + 32 * h]);
+        st_rec(recd + 4 * (int64_t)row, rc[h], qv[h], pc[h], dc[h]);
+        c.accum(acc, pc[h], rc[h], dc[h], qv[h]);
+      }
+    }
+  }
+}
+
 // Resident variant for latency-bound graphs (every warp owns <= kStages chunks,
 // DESIGN.md §5.3): the chunks' r, q, p, x, D^-1, shift and codes stay in this warp's
 // slots for the whole solve, so an iteration streams nothing; in-chunk neighbours read
@@ -962,9 +1118,11 @@ __device__ void iter_graph8(const Ctx& c, const ContDev& C, int r0, int r1,
 
 // ---------------------------------------------------------------- init pass
 // b = (m/tau) u + F + [D: sum sigma u_other];  r0 = b - K u;  x = u;  p0 = q0 = 0
+// recw: nullptr, or this row's 32-byte record {r, q, p, D^-1} of the streaming ELL pass
 template <bool CPL>
 __device__ __forceinline__ void init_row(const StepParams& P, int64_t gi, double Ku_nb,
-                                         const double* uo, double* x, int myphase, double (&acc)[3]) {
+                                         const double* uo, double* x, int myphase, double (&acc)[3],
+                                         double* recw = nullptr) {
   const double u = uo[gi];
   double b = ldro(P.mtau + gi) * u + ldro(P.F + gi);
   double Ku = ldro((CPL ? P.dsC : P.dsD) + gi) * u + Ku_nb;
@@ -987,13 +1145,18 @@ __device__ __forceinline__ void init_row(const StepParams& P, int64_t gi, double
     }
   }
   const double r = b - Ku;
+  const double di = ldro(P.dinv + gi);
   x[gi] = u;
-  stmut(P.r[0] + gi, r);
-  stmut(P.p[0] + gi, 0.0);
-  stmut(P.q[0] + gi, 0.0);
+  if (recw) {
+    st_rec(recw, r, 0.0, 0.0, di);
+  } else {
+    stmut(P.r[0] + gi, r);
+    stmut(P.p[0] + gi, 0.0);
+    stmut(P.q[0] + gi, 0.0);
+  }
   acc[0] += b * b;
   acc[1] += r * r;
-  acc[2] += ldro(P.dinv + gi) * r * r;
+  acc[2] += di * r * r;
 }
 
 template <bool CPL>
@@ -1024,7 +1187,7 @@ __device__ void init_item(const StepParams& P, const Item& it, const double* uo,
         const double t = C.val ? ldro(C.val + e) : C.Tconst;
         s += t * (u - uo[ldro(C.col + e)]);
       }
-      init_row<CPL>(P, gi, s, uo, x, myphase, acc);
+      init_row<CPL>(P, gi, s, uo, x, myphase, acc, (!CPL && C.rec[0]) ? C.rec[0] + 4 * (int64_t)i : nullptr);
     }
   }
 }
@@ -1749,6 +1912,7 @@ __device__ void run_group(const StepParams& P, int g, int cl, double* x, const d
       for (int k = 0; k < P.L; ++k)
         if (((G.cont_mask >> k) & 1) && P.cont[k].rr) {
           if (P.cont[k].resident) iter_ells_res<CPL>(c, P.cont[k], wg, W, st, j == 0, a5);
+          else if (!CPL && P.cont[k].rec[0]) iter_ells4(c, P.cont[k], wg, W, st, s, a5);
           else iter_ells<CPL>(c, P.cont[k], wg, W, st, a5);
         }
       for (int it = ib + wg; it < ie; it += W) {

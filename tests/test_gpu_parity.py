@@ -441,7 +441,7 @@ def test_config2_full_size_parity_D(torch_cuda):
 
 @pytest.mark.slow
 @pytest.mark.skipif(not os.environ.get("MC_LONG_TESTS"), reason="tens of minutes of CPU oracle; set MC_LONG_TESTS=1 "
-                    "(scripts/parity_full.py writes the committed record)")
+                    "(tests/tools/parity_full.py writes the committed record)")
 def test_config2_full_size_parity_coupled(torch_cuda):
     """Config 2 coupled, steps 1-2 (the 8.9M-row coupled CG oracle takes tens of minutes:
     slow-marked; the record is profiles/r02_parity_config2_coupled.json)."""

@@ -1,7 +1,7 @@
 #!/usr/bin/env python
 """Full-size parity record for the configs no sparse factorisation can take (2 and 4).
 
-    python scripts/parity_full.py --config 4 --scheme D --steps 2 --out profiles/r02_parity_config4_D.json
+    python tests/tools/parity_full.py --config 4 --scheme D --steps 2 --out profiles/r02_parity_config4_D.json
 
 Both sides run on the SAME box from the same seeded scenario (inputs.make): the CUDA path
 (libmc through the C ABI) steps the GPU, the C Jacobi-PCG oracle (oracle/fluxcg.py, rtol
@@ -23,7 +23,7 @@ import time
 
 import numpy as np
 
-ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 sys.path.insert(0, ROOT)
 
 CONFIG_RTOL = {0: None, 1: None, 2: None, 3: None, 4: [1e-13, 1e-12]}   # DESIGN.md C25
