@@ -57,6 +57,9 @@ def oracle_only(args):
         its = [i[-1] for i in st.iters] if args.scheme == "D" else [st.op.iters[-1]]
         meta["steps"].append({"step": n, "oracle_s": time.perf_counter() - t0, "oracle_iters": its})
         np.save(os.path.join(args.save, f"config{args.config}_{args.scheme}_step{n}.npy"), u)
+        if args.scheme == "D":
+            for a in range(lean.L):
+                np.save(os.path.join(args.save, f"config{args.config}_{args.scheme}_step{n}_c{a}.npy"), u[lean.block(a)])
         json.dump(meta, open(os.path.join(args.save, f"config{args.config}_{args.scheme}.json"), "w"), indent=1)
         print(json.dumps(meta["steps"][-1]), flush=True)
 
@@ -128,17 +131,42 @@ def main():
         tlast[0] = time.perf_counter()
 
     if args.load:
+        # D-scheme only: the oracle runs here except for the (step, continuum) solves whose
+        # result a --save run of the same oracle code left in DIR (the config-4 fracture solve
+        # takes about an hour on 8 cores; its 133 MB state ships with the repo snapshot, the
+        # 537 MB matrix states do not fit and are recomputed here).  The oracle is bitwise
+        # independent of the thread count (tests/test_oracle_fluxcg.py), so the mixed
+        # trajectory is the oracle's own.
+        assert args.scheme == "D"
         meta = json.load(open(os.path.join(args.load, f"config{args.config}_{args.scheme}.json")))
-        rec["oracle"].update(meta["oracle"], where="precomputed on another host by --save, states loaded from disk")
-        its = {r["step"]: r["oracle_iters"] for r in meta["steps"]}
-        secs = {r["step"]: r["oracle_s"] for r in meta["steps"]}
+        pre = {r["step"]: r for r in meta["steps"]}
+        st = fluxcg.DSchemeCG(lean, tau)
+        rec["oracle"]["precomputed"] = dict(meta["oracle"], what=[])
+        last_iters = [0] * lean.L
 
         def iters_of():
-            return [[i] for i in its[len(rec["steps"]) + 1]]
+            return [[i] for i in last_iters]
 
+        u = lean.u0.copy()
+        tlast[0] = time.perf_counter()
         for n in range(1, args.steps + 1):
-            u = np.load(os.path.join(args.load, f"config{args.config}_{args.scheme}_step{n}.npy"))
-            tlast[0] = time.perf_counter() - secs[n]
+            b = st.rhs(u)
+            new = np.empty_like(u)
+            for a in range(lean.L):
+                sl = lean.block(a)
+                f = os.path.join(args.load, f"config{args.config}_{args.scheme}_step{n}_c{a}.npy")
+                if os.path.exists(f):
+                    new[sl] = np.load(f)
+                    last_iters[a] = pre[n]["oracle_iters"][a]
+                    rec["oracle"]["precomputed"]["what"].append({"step": n, "continuum": a,
+                                                                 "oracle_s": pre[n]["oracle_s"]})
+                    # the shipped state solves THIS box's oracle system: true residual check
+                    res = float(np.linalg.norm(st.ops[a].apply(new[sl]) - b[sl]) / max(np.linalg.norm(b[sl]), 1e-300))
+                    rec["oracle"]["precomputed"]["what"][-1]["true_relres_on_this_box"] = res
+                else:
+                    new[sl] = st.ops[a].solve(b[sl], u[sl], 1e-13)
+                    last_iters[a] = st.ops[a].iters[-1]
+            u = new
             check(n, u)
     else:
         st = fluxcg.DSchemeCG(lean, tau) if args.scheme == "D" else fluxcg.CoupledCG(lean, tau)
