@@ -12,7 +12,9 @@
 //                       S = C Z and its dense Cholesky, psi^{i,beta} = Z S^{-1} e_(i,beta)
 //                       -- Eq. eq:basis by block elimination of the multipliers.
 //   nlmc_project_kernel one warp per pair of overlapping bases: psi_r^T D psi_s in flux
-//                       form (sum over connections T (dpsi_r)(dpsi_s) + boundary terms).
+//                       form (sum over connections T (dpsi_r)(dpsi_s) + boundary terms),
+//                       read from the per-region sparse storage the basis kernel wrote
+//                       (O(sum |K_i^+|) doubles; a window map per region finds psi_r(g)).
 // Host: Dbar in flux form (reading C32), Qbar, Wbar, Mbar, Fbar aggregated.
 #include <algorithm>
 #include <array>
@@ -42,6 +44,7 @@ struct NlDomain {
   int64_t cons0;                // constraint -> local DOF lists (CSR over kc rows)
   int32_t own0;                 // first own entry
   int32_t pad;
+  int64_t woff;                 // window map of K_i^+: (layer, fine y, fine x) -> local DOF or -1
 };
 
 struct NlParams {
@@ -68,9 +71,9 @@ struct NlParams {
 };
 
 // ---------------------------------------------------------------- basis kernel
-// One WARP per region K_i^+ (a few warps per CTA, persistent over regions): no CTA
-// barriers on the sequential paths, only __syncwarp.  Global rows the next steps need are
-// prefetched kWP rows ahead with cp.async into per-warp shared-memory rings.
+// One CTA per region K_i^+ at a time (persistent over regions; a one-warp-per-region
+// version measured 6x slower).  Global rows the next steps need are
+// prefetched kWP rows ahead with cp.async into shared-memory rings.
 __device__ __forceinline__ unsigned nl_smem(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
 __device__ __forceinline__ void nl_cp8(double* dst, const double* src) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(nl_smem(dst)), "l"(src) : "memory");
@@ -327,21 +330,17 @@ __global__ void __launch_bounds__(NT) nlmc_basis_kernel(const NlParams P) {
   }
 }
 
-// psi of every coarse DOF scattered into its dense fine vector
-__global__ void nlmc_scatter_kernel(const NlDomain* dom, const int32_t* dom_of, const int32_t* lglob,
-                                    const double* psi, const int64_t* psi_off, double* dense, int64_t N,
-                                    int64_t nH) {
-  for (int64_t r = blockIdx.x; r < nH; r += gridDim.x) {
-    const NlDomain D = dom[dom_of[r]];
-    for (int l = threadIdx.x; l < D.n; l += blockDim.x) dense[r * N + lglob[D.dof0 + l]] = psi[psi_off[r] + l];
-  }
-}
-
 // ---------------------------------------------------------------- projection kernel
 // Dbar(r, s) = psi_r^T D psi_s = sum over connections (a, b) T (psi_r(a) - psi_r(b)) *
 // (psi_s(a) - psi_s(b)) + sum_g ddiag_g psi_r(g) psi_s(g): one warp per pair, the
 // connections of the fine DOFs of K_{i(s)}^+ (each connection counted at its lower end
 // when both ends are inside, at the inside end otherwise).
+//
+// The bases stay in the per-region sparse storage the basis kernel wrote (psi[psi_off[r] +
+// l], l = local DOF of K_{i(r)}^+): O(sum |K_i^+|) doubles.  psi_r(g) for a global fine DOF
+// g is found through the region's window map: K_i^+ is a rectangle of fine cells, every
+// fine DOF has a host cell and a layer (its continuum; several graph cells of one continuum
+// in one host cell take successive layers), wmap[woff + (layer * wy + y) * wx + x] = l or -1.
 struct NlProj {
   int64_t npair;
   const int32_t* pr;            // pair -> coarse DOF r, s
@@ -349,16 +348,26 @@ struct NlProj {
   const int32_t* dom_of;        // coarse DOF -> domain
   const NlDomain* dom;
   const int32_t* lglob;
-  const double* dense;          // [n_coarse][N] scattered bases
-  int64_t N;
+  const double* psi;            // bases, per-region local numbering
+  const int64_t* psi_off;
+  const int32_t* wmap;
+  const int32_t* host;          // fine DOF -> host grid cell
+  const int32_t* layer;         // fine DOF -> window layer
+  int32_t nx, bx, by;
   const int32_t* arow;          // fine D in CSR (global): connections
   const int32_t* acol;
   const double* aval;
   const double* ddiag;
-  const int32_t* cell;          // coarse cell of every fine DOF
-  int32_t nHx;
   double* out;                  // [npair]
 };
+
+// local DOF of fine DOF (host cell (hx, hy), layer) in region D, or -1 when outside K_i^+
+__device__ __forceinline__ int nl_wloc(const NlProj& P, const NlDomain& D, int hx, int hy, int layer) {
+  const int x = hx - D.cx0 * P.bx, y = hy - D.cy0 * P.by;
+  const int wx = (D.cx1 - D.cx0 + 1) * P.bx, wy = (D.cy1 - D.cy0 + 1) * P.by;
+  if ((unsigned)x >= (unsigned)wx || (unsigned)y >= (unsigned)wy) return -1;
+  return P.wmap[D.woff + ((int64_t)layer * wy + y) * wx + x];
+}
 
 __global__ void nlmc_project_kernel(const NlProj P) {
   const int lane = threadIdx.x & 31;
@@ -367,22 +376,25 @@ __global__ void nlmc_project_kernel(const NlProj P) {
   for (int64_t pi = w; pi < P.npair; pi += nwarps) {
     const int r = P.pr[pi], s = P.ps[pi];
     const NlDomain Ds = P.dom[P.dom_of[s]];
-    const double* xr = P.dense + (size_t)r * P.N;
-    const double* xs = P.dense + (size_t)s * P.N;
+    const NlDomain Dr = P.dom[P.dom_of[r]];
+    const double* xr = P.psi + P.psi_off[r];
+    const double* xs = P.psi + P.psi_off[s];
     double acc = 0.0;
     for (int l = lane; l < Ds.n; l += 32) {
       const int g = P.lglob[Ds.dof0 + l];
-      const double rg = xr[g], sg = xs[g];
+      const int hc = P.host[g], gy = hc / P.nx, gx = hc - gy * P.nx;
+      const int lr = nl_wloc(P, Dr, gx, gy, P.layer[g]);
+      const double rg = lr >= 0 ? xr[lr] : 0.0, sg = xs[l];
       double v = P.ddiag[g] * rg * sg;
       for (int32_t e = P.arow[g]; e < P.arow[g + 1]; ++e) {
         const int h = P.acol[e];
-        const double sh = xs[h];
+        const int hh = P.host[h], hy = hh / P.nx, hx = hh - hy * P.nx, hl = P.layer[h];
+        const int ls = nl_wloc(P, Ds, hx, hy, hl);
         // count each connection once: at g if the other end h lies outside K_{i(s)}^+
         // (psi_s(h) = 0 there) or h > g
-        const int ch = P.cell[h], hy = ch / P.nHx, hx = ch % P.nHx;
-        const bool hin = hx >= Ds.cx0 && hx <= Ds.cx1 && hy >= Ds.cy0 && hy <= Ds.cy1;
-        if (!hin || h > g) {
-          const double d1 = rg - xr[h], d2 = sg - sh;
+        if (ls < 0 || h > g) {
+          const int lrh = nl_wloc(P, Dr, hx, hy, hl);
+          const double d1 = rg - (lrh >= 0 ? xr[lrh] : 0.0), d2 = sg - (ls >= 0 ? xs[ls] : 0.0);
           v = __fma_rn(P.aval[e] * d1, d2, v);
         }
       }
@@ -400,7 +412,7 @@ using namespace mc;
 
 struct mc_nlmc {
   ~mc_nlmc() {
-    if (d_dense) cudaFree(d_dense);
+    if (d_psi) cudaFree(d_psi);
   }
   std::string err;
   int L = 0;
@@ -410,7 +422,10 @@ struct mc_nlmc {
   std::vector<int32_t> fine_dof;
   std::vector<int32_t> rowptr, col;
   std::vector<double> val, mass, rhs, u0;
-  double* d_dense = nullptr;         // n_coarse x N bases (device)
+  double* d_psi = nullptr;           // bases in per-region local numbering (device), sum |K_i^+| x own DOFs
+  std::vector<int64_t> psi_off;      // coarse DOF -> its basis in d_psi
+  std::vector<int32_t> psi_dof0, psi_n;   // coarse DOF -> its region's slice of lglob
+  std::vector<int32_t> lglob;        // region-local DOF -> global fine DOF
   double ms_basis = 0.0, ms_project = 0.0;
 };
 
@@ -606,6 +621,27 @@ extern "C" mc_status mc_nlmc_build(mc_ctx* fine, const mc_nlmc_desc* d, mc_nlmc*
   std::vector<int32_t> loc((size_t)N, -1);
   int nmax = 1, bmax = 0, kcmax = 1;
   int64_t spw_need = 1;
+  // window layers: one per grid continuum; a graph continuum takes as many as its busiest
+  // host cell holds cells of it (1 when the host map is injective, e.g. merged fracture cells)
+  std::vector<int32_t> layer((size_t)N, 0), wmap;
+  int nlayers = 0;
+  {
+    std::vector<int32_t> seen;
+    for (int a = 0; a < L; ++a) {
+      int mult = 1;
+      if (fs.kind[(size_t)a] == 1) {
+        seen.assign((size_t)fs.nx * fs.ny, 0);
+        for (int64_t g = fs.off[(size_t)a]; g < fs.off[(size_t)a + 1]; ++g) {
+          const int32_t k = seen[(size_t)fs.host[(size_t)g]]++;
+          layer[(size_t)g] = nlayers + k;
+          mult = std::max(mult, k + 1);
+        }
+      } else {
+        for (int64_t g = fs.off[(size_t)a]; g < fs.off[(size_t)a + 1]; ++g) layer[(size_t)g] = nlayers;
+      }
+      nlayers += mult;
+    }
+  }
   for (int i = 0; i < nHx * nHy; ++i) {
     if (owned[(size_t)i].empty()) continue;
     const int iy = i / nHx, ix = i % nHx;
@@ -628,6 +664,16 @@ extern "C" mc_status mc_nlmc_build(mc_ctx* fine, const mc_nlmc_desc* d, mc_nlmc*
     D.dof0 = (int64_t)lglob.size();
     D.ent0 = (int64_t)erow.size();
     for (int l = 0; l < D.n; ++l) loc[(size_t)S[(size_t)l]] = l;
+    {
+      const int wx = (D.cx1 - D.cx0 + 1) * bx, wy = (D.cy1 - D.cy0 + 1) * by;
+      D.woff = (int64_t)wmap.size();
+      wmap.resize(wmap.size() + (size_t)nlayers * wx * wy, -1);
+      for (int l = 0; l < D.n; ++l) {
+        const int32_t g = S[(size_t)l], hc = fs.host[(size_t)g];
+        const int x = hc % fs.nx - D.cx0 * bx, y = hc / fs.nx - D.cy0 * by;
+        wmap[(size_t)(D.woff + ((int64_t)layer[(size_t)g] * wy + y) * wx + x)] = l;
+      }
+    }
     // constraints: coarse DOFs present in K_i^+ (ascending)
     std::vector<int32_t> cons;
     for (int32_t g : S) cons.push_back(fdof[(size_t)g]);
@@ -750,7 +796,8 @@ extern "C" mc_status mc_nlmc_build(mc_ctx* fine, const mc_nlmc_desc* d, mc_nlmc*
   P.z_stride = (int64_t)nmax * kcmax;
   NL_CUDA(B.alloc(&dband, (size_t)grid * wpb * P.band_stride));
   NL_CUDA(B.alloc(&dZ, (size_t)grid * wpb * P.z_stride));
-  NL_CUDA(B.alloc(&dpsi, (size_t)psi_len));
+  NL_CUDA(cudaMalloc(&dpsi, std::max<size_t>((size_t)psi_len, 1) * sizeof(double)));   // kept: the bases
+  nl->d_psi = dpsi;
   NL_CUDA(B.alloc(&derr, 1));
   NL_CUDA(cudaMemset(derr, 0, sizeof(int32_t)));
   P.dom = ddom;
@@ -797,19 +844,15 @@ extern "C" mc_status mc_nlmc_build(mc_ctx* fine, const mc_nlmc_desc* d, mc_nlmc*
     delete nl;
     return ctx_error(fine, MC_ERR_ARG, msg);
   }
-  // ---- scatter the bases into dense fine vectors (device), project
-  double* ddense;
-  NL_CUDA(cudaMalloc(&ddense, std::max<size_t>((size_t)nH * N, 1) * sizeof(double)));
-  nl->d_dense = ddense;
-  NL_CUDA(cudaMemset(ddense, 0, (size_t)nH * N * sizeof(double)));
-  {
-    int32_t* ddof;
-    int64_t* dpoff;
-    NL_CUDA(B.put(&ddof, dom_of));
-    NL_CUDA(B.put(&dpoff, psi_off));
-    nlmc_scatter_kernel<<<std::max<int64_t>(1, std::min<int64_t>(nH, 4 * sms)), 256>>>(ddom, ddof, dlglob, dpsi, dpoff,
-                                                                                        ddense, N, nH);
-    NL_CUDA(cudaGetLastError());
+  // ---- the bases stay in their per-region storage (dpsi); project from it
+  nl->psi_off = psi_off;
+  nl->lglob = lglob;
+  nl->psi_dof0.resize((size_t)nH);
+  nl->psi_n.resize((size_t)nH);
+  for (int64_t r = 0; r < nH; ++r) {
+    const NlDomain& Dr = dom[(size_t)dom_of[(size_t)r]];
+    nl->psi_dof0[(size_t)r] = (int32_t)Dr.dof0;
+    nl->psi_n[(size_t)r] = Dr.n;
   }
   // pairs (r <= s) whose regions overlap
   std::vector<int32_t> pr, ps;
@@ -822,7 +865,8 @@ extern "C" mc_status mc_nlmc_build(mc_ctx* fine, const mc_nlmc_desc* d, mc_nlmc*
       }
     }
   NlProj Q{};
-  int32_t *dpr, *dps, *ddom_of, *darow, *dacol, *dcell;
+  int32_t *dpr, *dps, *ddom_of, *darow, *dacol, *dwmap, *dhost, *dlayer;
+  int64_t* dpoff;
   double *daval, *dddiag, *dout;
   NL_CUDA(B.put(&dpr, pr));
   NL_CUDA(B.put(&dps, ps));
@@ -831,7 +875,10 @@ extern "C" mc_status mc_nlmc_build(mc_ctx* fine, const mc_nlmc_desc* d, mc_nlmc*
   NL_CUDA(B.put(&dacol, acol));
   NL_CUDA(B.put(&daval, aval));
   NL_CUDA(B.put(&dddiag, fs.ddiag));
-  NL_CUDA(B.put(&dcell, cell));
+  NL_CUDA(B.put(&dwmap, wmap));
+  NL_CUDA(B.put(&dhost, fs.host));
+  NL_CUDA(B.put(&dlayer, layer));
+  NL_CUDA(B.put(&dpoff, psi_off));
   NL_CUDA(B.alloc(&dout, pr.size()));
   Q.npair = (int64_t)pr.size();
   Q.pr = dpr;
@@ -839,14 +886,18 @@ extern "C" mc_status mc_nlmc_build(mc_ctx* fine, const mc_nlmc_desc* d, mc_nlmc*
   Q.dom_of = ddom_of;
   Q.dom = ddom;
   Q.lglob = dlglob;
-  Q.dense = ddense;
-  Q.N = N;
+  Q.psi = dpsi;
+  Q.psi_off = dpoff;
+  Q.wmap = dwmap;
+  Q.host = dhost;
+  Q.layer = dlayer;
+  Q.nx = fs.nx;
+  Q.bx = bx;
+  Q.by = by;
   Q.arow = darow;
   Q.acol = dacol;
   Q.aval = daval;
   Q.ddiag = dddiag;
-  Q.cell = dcell;
-  Q.nHx = nHx;
   Q.out = dout;
   cudaEvent_t e3;
   NL_CUDA(cudaEventCreate(&e3));
@@ -949,10 +1000,16 @@ extern "C" mc_status mc_nlmc_get(const mc_nlmc* nl, int32_t* rowptr, int32_t* co
 
 extern "C" mc_status mc_nlmc_basis(const mc_nlmc* nl, int64_t r, double* psi) {
   if (!nl || !psi || r < 0 || r >= nl->nH) return MC_ERR_ARG;
-  return cudaMemcpy(psi, nl->d_dense + (size_t)r * nl->N, (size_t)nl->N * sizeof(double), cudaMemcpyDefault) ==
-                 cudaSuccess
-             ? MC_OK
-             : MC_ERR_CUDA;
+  // expand the region-local basis into a fine vector (zero outside K_i^+)
+  const int32_t n = nl->psi_n[(size_t)r];
+  std::vector<double> loc((size_t)n), out((size_t)nl->N, 0.0);
+  if (cudaMemcpy(loc.data(), nl->d_psi + nl->psi_off[(size_t)r], (size_t)n * sizeof(double), cudaMemcpyDeviceToHost) !=
+      cudaSuccess)
+    return MC_ERR_CUDA;
+  const int32_t* lg = nl->lglob.data() + nl->psi_dof0[(size_t)r];
+  for (int32_t l = 0; l < n; ++l) out[(size_t)lg[l]] = loc[(size_t)l];
+  return cudaMemcpy(psi, out.data(), (size_t)nl->N * sizeof(double), cudaMemcpyDefault) == cudaSuccess ? MC_OK
+                                                                                                      : MC_ERR_CUDA;
 }
 
 extern "C" mc_status mc_nlmc_times(const mc_nlmc* nl, double* ms_basis, double* ms_project) {
