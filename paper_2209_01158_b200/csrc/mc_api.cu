@@ -36,6 +36,8 @@ using namespace mc;
 namespace {
 
 constexpr int64_t kLargeRows = int64_t(2) << 20;   // "bandwidth-bound" solve
+constexpr size_t kGuardBytes = 256;
+constexpr int kGuardByte = 0xA5;
 constexpr int kPlanSteps = 3;                        // D-scheme steps after which the CTA plan is frozen
 constexpr int kRunBatch = 256;                       // mc_run: steps enqueued per synchronisation
 constexpr int64_t kOneCtaWork = 0;                   // rows + stored entries below which a solve gets one CTA
@@ -135,6 +137,7 @@ struct mc_ctx {
   bool has_korder = false;
   int uploaded_plan = -1;                       // scheme whose items are on device
   std::vector<void*> allocs;
+  std::vector<std::pair<void*, size_t>> guards;   // MC_CHECK builds: (array, bytes) with guard bytes behind
 };
 
 static std::string g_create_err;
@@ -163,7 +166,15 @@ mc_status fail(mc_ctx* c, mc_status st, const char* fmt, ...) {
 template <class T>
 mc_status dev_alloc(mc_ctx* c, T** p, size_t count) {
   void* v = nullptr;
-  CUDA_TRY(c, cudaMalloc(&v, std::max<size_t>(count, 1) * sizeof(T)));
+  const size_t bytes = std::max<size_t>(count, 1) * sizeof(T);
+#if MC_CHECK
+  // checked build: 256 guard bytes after every device array, verified by mc_debug_check
+  CUDA_TRY(c, cudaMalloc(&v, bytes + kGuardBytes));
+  CUDA_TRY(c, cudaMemset(static_cast<char*>(v) + bytes, kGuardByte, kGuardBytes));
+  c->guards.emplace_back(v, bytes);
+#else
+  CUDA_TRY(c, cudaMalloc(&v, bytes));
+#endif
   c->allocs.push_back(v);
   *p = static_cast<T*>(v);
   return MC_OK;
@@ -272,6 +283,27 @@ extern "C" mc_status mc_destroy(mc_ctx* c) {
   delete c;
   return MC_OK;
 }
+
+#if MC_CHECK
+// checked build only (libmc_check.so, not declared in include/mc.h): number of device arrays
+// whose guard bytes were overwritten -- an out-of-bounds write of some kernel
+extern "C" int32_t mc_debug_check(mc_ctx* c) {
+  if (!c) return -1;
+  if (cudaStreamSynchronize(c->stream) != cudaSuccess) return -2;
+  int32_t bad = 0;
+  std::vector<unsigned char> h(kGuardBytes);
+  for (auto& g : c->guards) {
+    if (cudaMemcpy(h.data(), static_cast<char*>(g.first) + g.second, kGuardBytes, cudaMemcpyDeviceToHost) != cudaSuccess)
+      return -2;
+    for (unsigned char b : h)
+      if (b != (unsigned char)kGuardByte) {
+        ++bad;
+        break;
+      }
+  }
+  return bad;
+}
+#endif
 
 extern "C" int64_t mc_size(const mc_ctx* c, int32_t alpha) {
   if (!c) return -1;
@@ -1182,6 +1214,11 @@ static mc_status enqueue_step(mc_ctx* c, int scheme, mc_step_report* rep_dev, cu
         cudaStreamSynchronize(c->stream);
         cudaFree(c->items);
         c->allocs.erase(std::find(c->allocs.begin(), c->allocs.end(), (void*)c->items));
+        for (size_t gi = 0; gi < c->guards.size(); ++gi)
+          if (c->guards[gi].first == (void*)c->items) {
+            c->guards.erase(c->guards.begin() + (long)gi);
+            break;
+          }
         c->items = nullptr;
       }
       mc_status st = dev_alloc(c, &c->items, cp.items.size() * 2);

@@ -18,6 +18,17 @@ constexpr int kWarps = kThreads / 32;
 #ifndef MC_PROF
 #define MC_PROF 0                          // dev: per-phase clock64 instrumentation (mc_prof_read)
 #endif
+#ifndef MC_CHECK
+#define MC_CHECK 0                         // checked build (libmc_check.so): device-side bounds asserts on every
+#endif                                     // gather index, staged window and work item; guard words after every
+                                           // device array verified at mc_destroy.  compute-sanitizer is closed
+                                           // on the B200 pool, this is its stand-in.
+#if MC_CHECK
+#include <cassert>
+#define MC_ASSERT(c) assert(c)
+#else
+#define MC_ASSERT(c) ((void)0)
+#endif
 #ifndef MC_TMA
 #define MC_TMA 1                           // stage with TMA bulk copies (1) or per-lane cp.async (0)
 #endif

@@ -99,10 +99,12 @@ struct Ctx {
   double a, b;
 
   __device__ __forceinline__ double pn_at(int64_t gi) const {
+    MC_ASSERT(gi >= 0 && gi < P->N);
     return pnew(ldnb(rs + gi), ldnb(qs + gi), ldnb(ps + gi), ldro(P->dinv + gi), a, b);
   }
   // owner update of row gi: x, r, p stored; returns p_j, r_j, D^{-1}_ii
   __device__ __forceinline__ void own(int64_t gi, double& pn, double& rn, double& di) const {
+    MC_ASSERT(gi >= 0 && gi < P->N);
     const double ro = ldmut(rs + gi), qo = ldmut(qs + gi), po = ldmut(ps + gi);
     di = ldro(P->dinv + gi);
     const double xo = x[gi];
@@ -115,6 +117,7 @@ struct Ctx {
   __device__ __forceinline__ double couple_q(int64_t gi, double pc) const {
     double acc = 0.0;
     const int32_t e0 = ldro(P->cptr + gi), e1 = ldro(P->cptr + gi + 1);
+    MC_ASSERT(e0 <= e1);
     for (int32_t e = e0; e < e1; ++e) {
       const int32_t j = ldro(P->cidx + e);
       acc += ldro(P->cval + e) * (pc - pn_at(j));
@@ -306,6 +309,7 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
 }
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+  MC_ASSERT((reinterpret_cast<uintptr_t>(src) & 15) == 0 && (smem_u32(dst) & 15) == 0 && (bytes & 15) == 0 && bytes > 0);
   asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
                    smem_u32(dst)),
                "l"(src), "r"(bytes), "r"(smem_u32(bar))
@@ -581,6 +585,7 @@ __device__ __forceinline__ FarG far_gather(const Ctx& c, const double* sl, int l
         ++nfar;
       }
   f.w0 = f.w1 = f.w2 = f.w3 = 0.0;
+  MC_ASSERT(i0 < c.P->N && i1 < c.P->N && i2 < c.P->N && i3 < c.P->N);
   if (i0 >= 0) f.w0 = c.pn_at(i0);
   if (i1 >= 0) f.w1 = c.pn_at(i1);
   if (i2 >= 0) f.w2 = c.pn_at(i2);
@@ -674,6 +679,7 @@ __device__ void iter_ells(const Ctx& c, const ContDev& C, int wg, int W, const S
       for (int k = 0; k < 4; ++k) {
         const int32_t cd = j[h][k];
         double v = pc[h];                                          // -1: no neighbour
+        MC_ASSERT(cd >= -2 - 67);
         if (cd <= -2) v = pnb[-2 - cd];
         else if (cd >= 0) {
           if (fcur.s0 == 4 * h + k) v = fcur.w0;
@@ -1129,6 +1135,7 @@ __device__ __forceinline__ void init_row(const StepParams& P, int64_t gi, double
   const int32_t e0 = ldro(P.cptr + gi), e1 = ldro(P.cptr + gi + 1);
   for (int32_t e = e0; e < e1; ++e) {
     const int32_t j = ldro(P.cidx + e);
+    MC_ASSERT(j >= 0 && j < P.N);
     const double s = ldro(P.cval + e);
     if (CPL) {
       Ku += s * (u - uo[j]);
@@ -1162,7 +1169,9 @@ __device__ __forceinline__ void init_row(const StepParams& P, int64_t gi, double
 template <bool CPL>
 __device__ void init_item(const StepParams& P, const Item& it, const double* uo, double* x, int myphase,
                           double (&acc)[3]) {
+  MC_ASSERT(it.cont >= 0 && it.cont < P.L);
   const ContDev& C = P.cont[it.cont];
+  MC_ASSERT(it.kind == ITEM_GRID ? (it.a >= 0 && it.b >= 0 && it.c <= C.ny && it.b <= it.c) : (it.a >= 0 && it.b <= C.n));
   const int lane = threadIdx.x & 31;
   if (it.kind == ITEM_GRID) {
     const int nx = C.nx, ny = C.ny;
@@ -1214,6 +1223,7 @@ __device__ __forceinline__ void group_allreduce(const StepParams& P, int g, int 
   __shared__ double tot[kNPart];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int G = P.grp[g].cta_count, base = P.grp[g].cta_begin;
+  MC_ASSERT(cl >= 0 && cl < G && base + G <= P.total_ctas);
   const int eb = (int)(epoch & 1ull);
 #pragma unroll
   for (int k = 0; k < NP; ++k) {

@@ -1,5 +1,9 @@
-"""compute-sanitizer target: a few steps of one case through the C ABI.
+"""Checked-build / compute-sanitizer target: a few steps of one case
+through the C ABI.
+    MC_LIB=paper_2209_01158_b200/libmc_check.so python scripts/sanitize_target.py CASE
     compute-sanitizer --tool memcheck python scripts/sanitize_target.py CASE
+With the checked build (-DMC_CHECK=1: device-side bounds asserts, guard bytes behind every
+device array) the script ends by calling mc_debug_check and fails on a corrupted guard.
 Cases: cfg0 (config 0, D + coupled + U), cfg3 (config 3 NLMC operator, D + coupled),
 ell_stream (config-1 recipe at 256^2 with 4 CTAs: the streaming Jacobi ELL pass),
 bjs (paper analogue, block-Jacobi, 4 CTAs: the streaming block-Jacobi passes), bj (resident),
@@ -51,5 +55,9 @@ elif case == "nlmc":
 else:
     raise SystemExit(f"unknown case {case}")
 torch.cuda.synchronize()
+if hasattr(pb.lib, "mc_debug_check"):
+    bad = pb.lib.mc_debug_check(pb.ctx)
+    print(case, "guards corrupted:", bad, flush=True)
+    assert bad == 0, bad
 pb.close()
 print(case, "done", flush=True)
