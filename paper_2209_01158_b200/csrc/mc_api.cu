@@ -104,7 +104,8 @@ struct mc_ctx {
   double* val[MC_MAX_CONTINUA] = {nullptr};
   int32_t* ecol[MC_MAX_CONTINUA] = {nullptr};
   int32_t* perm[MC_MAX_CONTINUA] = {nullptr};   // graph: internal -> caller numbering
-  double* rec[MC_MAX_CONTINUA][2] = {{nullptr, nullptr}};   // streaming ELL pass: {r, q, p, D^-1} records
+  double* bstat[MC_MAX_CONTINUA] = {nullptr};                // chunk-blocked streaming ELL pass: static blocks
+  double* bdyn[MC_MAX_CONTINUA][2] = {{nullptr, nullptr}};   //   and CG-state blocks (allocated on first use)
   double* tinv[MC_MAX_CONTINUA] = {nullptr};    // bj: chunk Thomas factors
   double* tcp[MC_MAX_CONTINUA] = {nullptr};
   double* tem[MC_MAX_CONTINUA] = {nullptr};
@@ -904,6 +905,31 @@ static mc_status finalize(mc_ctx* c) {
           }
         }
         UP(c->ecol[a], ell);
+        if (!H.bj) {
+          // chunk-blocked static data of the streaming pass (iter_ellb): per 64-row chunk
+          // D^-1 (64) | D-scheme shift (64) | int32 codes [64][4], far neighbours first
+          const int64_t nchk = (H.n + 63) / 64;
+          std::vector<double> bst((size_t)nchk * kBStat, 0.0);
+          for (int64_t m = 0; m < nchk; ++m) {
+            int32_t* cp = reinterpret_cast<int32_t*>(&bst[(size_t)(m * kBStat + 128)]);
+            for (int q = 0; q < 256; ++q) cp[q] = -1;
+          }
+          for (int64_t i = 0; i < H.n; ++i) {
+            const int64_t m = i >> 6, w = i & 63;
+            const size_t g = (size_t)(c->off[a] + i);
+            bst[(size_t)(m * kBStat + w)] = dinv[g];
+            bst[(size_t)(m * kBStat + 64 + w)] = dsD[g];
+            int32_t* cp = reinterpret_cast<int32_t*>(&bst[(size_t)(m * kBStat + 128)]) + 4 * w;
+            int k = 0;
+            for (int pass = 0; pass < 2; ++pass)                 // far neighbours first
+              for (int32_t e = H.rowptr[(size_t)i]; e < H.rowptr[(size_t)i + 1]; ++e) {
+                const int64_t j = H.col[(size_t)e];
+                const bool far = (j >> 6) != m;
+                if (far == (pass == 0)) cp[k++] = far ? (int32_t)j : (int32_t)(-2 - (j & 63));
+              }
+          }
+          UP(c->bstat[a], bst);
+        }
         if (H.bj) {
           // block-Jacobi: tridiagonal part of every 64-row chunk (rows i, i+1 of the
           // chunk connected along the chain-ordered network), factored once (Thomas)
@@ -1043,10 +1069,10 @@ static int64_t one_cta_work() {
   return w;
 }
 
-// MC_RECORDS=0 (dev): keep the streaming ELL pass on the separate r, q, p arrays
-static bool use_records() {
+// MC_BLOCKED=0 (dev, A/B): keep the streaming ELL pass on the separate r, q, p arrays
+static bool use_blocked() {
   static const bool v = [] {
-    const char* e = getenv("MC_RECORDS");
+    const char* e = getenv("MC_BLOCKED");
     return !(e && e[0] == '0');
   }();
   return v;
@@ -1264,19 +1290,21 @@ static mc_status enqueue_step(mc_ctx* c, int scheme, mc_step_report* rep_dev, cu
         P.cont[a].bj = (nconts == 1 && nch <= (int64_t)G.cta_count * kWarps && c->tinv[a] != nullptr &&
                         scheme != MC_COUPLED) ? 1 : 0;
         P.cont[a].bjs = (!P.cont[a].bj && nconts == 1 && c->tinv[a] != nullptr && scheme != MC_COUPLED) ? 1 : 0;
-        // streaming Jacobi pass of a decoupled solve: CG state as 32-byte records (allocated
-        // the first time a plan streams this network)
-        if (use_records() && nconts == 1 && scheme != MC_COUPLED && !P.cont[a].resident && !P.cont[a].bj && !P.cont[a].bjs) {
-          if (!c->rec[a][0]) {
-            const size_t cnt = (size_t)4 * ((size_t)c->hc[a].n + 64 + kSlack);
+        // streaming Jacobi pass of a decoupled solve: chunk-blocked workspace (the CG-state
+        // blocks are allocated the first time a plan streams this network)
+        if (use_blocked() && c->bstat[a] && nconts == 1 && scheme != MC_COUPLED && !P.cont[a].resident &&
+            !P.cont[a].bj && !P.cont[a].bjs) {
+          if (!c->bdyn[a][0]) {
+            const size_t cnt = (size_t)((c->hc[a].n + 63) / 64) * kBDyn;
             for (int k = 0; k < 2; ++k) {
-              mc_status st = dev_alloc(c, &c->rec[a][k], cnt);
+              mc_status st = dev_alloc(c, &c->bdyn[a][k], cnt);
               if (st != MC_OK) return st;
-              CUDA_TRY(c, cudaMemsetAsync(c->rec[a][k], 0, cnt * 8, c->stream));
+              CUDA_TRY(c, cudaMemsetAsync(c->bdyn[a][k], 0, cnt * 8, c->stream));
             }
           }
-          P.cont[a].rec[0] = c->rec[a][0];
-          P.cont[a].rec[1] = c->rec[a][1];
+          P.cont[a].bstat = c->bstat[a];
+          P.cont[a].bdyn[0] = c->bdyn[a][0];
+          P.cont[a].bdyn[1] = c->bdyn[a][1];
         }
       }
   }

@@ -62,19 +62,6 @@ __device__ __forceinline__ double pnew(double ro, double qo, double po, double d
   return __fma_rn(di, rn, __dmul_rn(b, po));
 }
 
-// 32-byte CG-state records {r, q, p, D^-1} of the streaming ELL pass: one 256-bit access each
-__device__ __forceinline__ void st_rec(double* rec, double r, double q, double p, double d) {
-  asm volatile("st.global.cg.v4.f64 [%0], {%1,%2,%3,%4};" ::"l"(rec), "d"(r), "d"(q), "d"(p), "d"(d) : "memory");
-}
-struct Rec4 {
-  double r, q, p, d;
-};
-__device__ __forceinline__ Rec4 ld_rec(const double* rec) {
-  Rec4 v;
-  asm volatile("ld.global.cg.v4.f64 {%0,%1,%2,%3}, [%4];" : "=d"(v.r), "=d"(v.q), "=d"(v.p), "=d"(v.d) : "l"(rec) : "memory");
-  return v;
-}
-
 #if MC_PROF
 // dev instrumentation (-DMC_PROF=1 builds only): clock64 per phase of the CG loop,
 // summed over iterations by thread 0 of each group's first CTA
@@ -700,145 +687,108 @@ __device__ void iter_ells(const Ctx& c, const ContDev& C, int wg, int W, const S
   }
 }
 
-// Streaming ELL pass on 32-byte records (Jacobi, D-scheme).  Same sweep
-// and arithmetic as iter_ells, but the CG state of the network lives in records
-// {r, q, p, D^-1} per row (C.rec[s], double-buffered by iteration parity):
-//   * the chunk window (64 rows + 2-row halos) arrives with ONE bulk copy of 2 176 B;
-//   * a far neighbour costs ONE 256-bit load of one 32-byte sector instead of four 8-byte
-//     loads from four arrays (four sectors) -- the far gathers of the vertical segments
-//     were the pass's L2 -> SM traffic (128 of 192 B per row);
-//   * the new record leaves with one 256-bit store per row.
-// Lane l owns rows l and l + 32 of the chunk (records 32 B apart: 2-way bank conflicts on
-// the 128-bit shared loads instead of 4-way with rows 2l, 2l + 1).
-struct FarR {
-  double w0, w1, w2, w3;
-  int s0, s1, s2, s3;
-};
-
-__device__ __forceinline__ void ell_codes_r(const double* sl, int lane, int32_t (&j)[2][4]) {
-  const int32_t* si = reinterpret_cast<const int32_t*>(sl + 400);
-#pragma unroll
-  for (int h = 0; h < 2; ++h)
-#pragma unroll
-    for (int k = 0; k < 4; ++k) j[h][k] = si[k * 64 + lane + 32 * h];
+// Chunk-blocked streaming ELL pass (decoupled Jacobi solve of a network too large to stay
+// resident: configs 2 and 4).  Same sweep and arithmetic as iter_ells, on a
+// private layout in which everything a 64-row chunk needs is contiguous:
+//   bstat[m]   256 doubles  D^-1 (64) | shift (64) | int32 codes [64 rows][4]
+//   bdyn[s][m] 192 doubles  r (64) | q (64) | p (64)          (s = iteration parity)
+//   x          the state vector itself (64 doubles at the chunk's rows)
+// so a chunk arrives with THREE bulk copies (2048 + 1536 + 512 B) instead of ten, and the
+// pass issues ~3x fewer instructions per chunk than iter_ells (whose 715 instructions per
+// chunk made it co-limited by instruction issue: profiles/r02_fracture_only_soa.txt).
+// Codes (host, finalize): -1 none, -2 - w: row w of this chunk, >= 0: continuum-local row
+// of a neighbour in another chunk ("far": gathered from the previous iteration's r, q, p).
+// Far neighbours come first in a row's four slots, so only slots 0 and 1 are gathered in
+// the common batch; rows with three or four far neighbours take a warp-uniform extra step.
+__device__ __forceinline__ double pn_blk(const double* dyn, const double* stat, int32_t j, double a, double b) {
+  const int64_t blk = j >> 6;
+  const int w = j & 63;
+  const double* d = dyn + blk * kBDyn + w;
+  return pnew(ldnb(d), ldnb(d + 64), ldnb(d + 128), ldro(stat + blk * kBStat + w), a, b);
 }
 
-__device__ __forceinline__ double pn_rec(const Rec4& v, double a, double b) { return pnew(v.r, v.q, v.p, v.d, a, b); }
-
-__device__ void iter_ells4(const Ctx& c, const ContDev& C, int wg, int W, const Stage& st, int s,
-                           double (&acc)[kNPart]) {
+__device__ void iter_ellb(const Ctx& c, const ContDev& C, int wg, int W, const Stage& st, int s,
+                          double (&acc)[kNPart]) {
   double* wsm = st.wsm;
-  double* pnb = wsm + kWarpSmem - kPnBuf;                      // new p of the window rows
+  double* pnb = wsm + kWarpSmem - kPnBuf;                      // new p of the chunk's rows
   const int lane = threadIdx.x & 31;
-  const int64_t off = C.off, es = C.estride;
   const int r1 = (int)C.n;
   const int nch = (r1 + 63) / 64;
-  const double* recs = C.rec[s];
-  double* recd = C.rec[s ^ 1];
-  auto tix = [&](int m) { return (m / W) % kStagesE; };
-  auto prefetch = [&](int m) {
-    const int t = tix(m);
+  const double* stat = C.bstat;
+  const double* dyns = C.bdyn[s];
+  double* dynd = C.bdyn[s ^ 1];
+  double* xg = c.x + C.off;
+  auto prefetch = [&](int m, int t) {
     double* sl = wsm + t * kSlotE;
     __syncwarp();
     if (lane == 0) {
-      const int64_t b = 64 * (int64_t)m;
-      const bool full = b >= 2;                                 // window start in bounds
-      const unsigned wb = full ? 68u * 32u : 66u * 32u;
-      st.begin(t, wb + 2u * 512u + 4u * 256u);
+      st.begin(t, 8u * (kBStat + kBDyn + 64));
       uint64_t* bar = st.bars + t;
-      bulk_g2s(sl + (full ? 0 : 8), recs + 4 * (b - (full ? 2 : 0)), wb, bar);
-      bulk_g2s(sl + 272, c.x + off + b, 512, bar);
-      bulk_g2s(sl + 336, c.ds + off + b, 512, bar);
-      int32_t* si = reinterpret_cast<int32_t*>(sl + 400);
-#pragma unroll
-      for (int k = 0; k < 4; ++k) bulk_g2s(si + k * 64, C.ecol + k * es + b, 256, bar);
+      bulk_g2s(sl, stat + (int64_t)m * kBStat, 8u * kBStat, bar);
+      bulk_g2s(sl + kBStat, dyns + (int64_t)m * kBDyn, 8u * kBDyn, bar);
+      bulk_g2s(sl + kBStat + kBDyn, xg + 64 * (int64_t)m, 512, bar);
     }
   };
   if (wg >= nch) return;
-  prefetch(wg);
-  for (int m = wg; m < nch; m += W) {
-    if (m + W < nch) prefetch(m + W);                             // next chunk in flight
-    st.wait(tix(m));
-    const double* sl = wsm + tix(m) * kSlotE;
-    int32_t j[2][4];
-    ell_codes_r(sl, lane, j);
-    // far neighbours of this lane's two rows: up to 4 records gathered in one batch
-    FarR f;
-    f.s0 = f.s1 = f.s2 = f.s3 = -1;
-    int32_t i0 = -1, i1 = -1, i2 = -1, i3 = -1;
-    {
-      int nfar = 0;
-#pragma unroll
-      for (int h = 0; h < 2; ++h)
-#pragma unroll
-        for (int k = 0; k < 4; ++k)
-          if (j[h][k] >= 0) {
-            if (nfar == 0) {
-              i0 = j[h][k];
-              f.s0 = 4 * h + k;
-            } else if (nfar == 1) {
-              i1 = j[h][k];
-              f.s1 = 4 * h + k;
-            } else if (nfar == 2) {
-              i2 = j[h][k];
-              f.s2 = 4 * h + k;
-            } else if (nfar == 3) {
-              i3 = j[h][k];
-              f.s3 = 4 * h + k;
-            }
-            ++nfar;
-          }
-    }
-    f.w0 = f.w1 = f.w2 = f.w3 = 0.0;
-    if (i0 >= 0) f.w0 = pn_rec(ld_rec(recs + 4 * ((int64_t)i0 - off)), c.a, c.b);
-    if (i1 >= 0) f.w1 = pn_rec(ld_rec(recs + 4 * ((int64_t)i1 - off)), c.a, c.b);
-    if (i2 >= 0) f.w2 = pn_rec(ld_rec(recs + 4 * ((int64_t)i2 - off)), c.a, c.b);
-    if (i3 >= 0) f.w3 = pn_rec(ld_rec(recs + 4 * ((int64_t)i3 - off)), c.a, c.b);
-    const int base = 64 * m;
-    double pc[2], rc[2], dc[2], po[2];
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      const int w = 2 + lane + 32 * h;
-      const double2 rq = *reinterpret_cast<const double2*>(sl + 4 * w);
-      const double2 pd = *reinterpret_cast<const double2*>(sl + 4 * w + 2);
-      rc[h] = __fma_rn(-c.a, rq.y, rq.x);
-      dc[h] = pd.y;
-      po[h] = pd.x;
-      pc[h] = __fma_rn(dc[h], rc[h], __dmul_rn(c.b, po[h]));
-    }
+  prefetch(wg, 0);
+  int t = 0;
+  for (int m = wg; m < nch; m += W, t ^= 1) {
+    if (m + W < nch) prefetch(m + W, t ^ 1);                      // next chunk in flight
+    st.wait(t);
+    const double* sl = wsm + t * kSlotE;
+    // codes of rows 2 lane, 2 lane + 1: 8 consecutive int32
+    const int4 c0 = *reinterpret_cast<const int4*>(sl + 128 + 4 * lane);
+    const int4 c1 = *reinterpret_cast<const int4*>(sl + 128 + 4 * lane + 2);
+    // far neighbours (slots 0, 1 of each row): gathered in one batch, loads predicated per lane
+    double f00 = 0.0, f01 = 0.0, f10 = 0.0, f11 = 0.0;
+    if (c0.x >= 0) f00 = pn_blk(dyns, stat, c0.x, c.a, c.b);
+    if (c0.y >= 0) f01 = pn_blk(dyns, stat, c0.y, c.a, c.b);
+    if (c1.x >= 0) f10 = pn_blk(dyns, stat, c1.x, c.a, c.b);
+    if (c1.y >= 0) f11 = pn_blk(dyns, stat, c1.y, c.a, c.b);
+    const double2 di = *reinterpret_cast<const double2*>(sl + 2 * lane);
+    const double2 ds = *reinterpret_cast<const double2*>(sl + 64 + 2 * lane);
+    const double2 ro = *reinterpret_cast<const double2*>(sl + kBStat + 2 * lane);
+    const double2 qo = *reinterpret_cast<const double2*>(sl + kBStat + 64 + 2 * lane);
+    const double2 po = *reinterpret_cast<const double2*>(sl + kBStat + 128 + 2 * lane);
+    const double2 xo = *reinterpret_cast<const double2*>(sl + kBStat + kBDyn + 2 * lane);
+    const double r0 = __fma_rn(-c.a, qo.x, ro.x), r1n = __fma_rn(-c.a, qo.y, ro.y);
+    const double p0 = __fma_rn(di.x, r0, __dmul_rn(c.b, po.x)), p1 = __fma_rn(di.y, r1n, __dmul_rn(c.b, po.y));
     __syncwarp();                                                 // previous chunk's pnb reads done
-    pnb[2 + lane] = pc[0];
-    pnb[34 + lane] = pc[1];
-    if (lane < 4) {                                               // halo rows 0, 1, 66, 67
-      const int w = lane < 2 ? lane : 64 + lane;
-      pnb[w] = pnew(sl[4 * w], sl[4 * w + 1], sl[4 * w + 2], sl[4 * w + 3], c.a, c.b);
-    }
+    *reinterpret_cast<double2*>(pnb + 2 * lane) = make_double2(p0, p1);
     __syncwarp();
-    double qv[2];
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      double sum = 0.0;
-#pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        const int32_t cd = j[h][k];
-        double v = pc[h];                                          // -1: no neighbour
-        if (cd <= -2) v = pnb[-2 - cd];
-        else if (cd >= 0) {
-          if (f.s0 == 4 * h + k) v = f.w0;
-          else if (f.s1 == 4 * h + k) v = f.w1;
-          else if (f.s2 == 4 * h + k) v = f.w2;
-          else if (f.s3 == 4 * h + k) v = f.w3;
-          else v = pn_rec(ld_rec(recs + 4 * ((int64_t)cd - off)), c.a, c.b);   // rare: > 4 far in this lane
-        }
-        sum += pc[h] - v;
-      }
-      const int row = base + lane + 32 * h;
-      qv[h] = sl[336 + lane + 32 * h] * pc[h] + C.Tconst * sum;
-      if (row < r1) {
-        c.x[off + row] = __fma_rn(c.a, po[h], sl[272 + lane + 32 * h]);
-        st_rec(recd + 4 * (int64_t)row, rc[h], qv[h], pc[h], dc[h]);
-        c.accum(acc, pc[h], rc[h], dc[h], qv[h]);
-      }
+    // v(code, far value, own p): the neighbour's new p
+    auto nbv = [&](int32_t cd, double far, double own) { return cd >= 0 ? far : (cd <= -2 ? pnb[-2 - cd] : own); };
+    double f02 = 0.0, f03 = 0.0, f12 = 0.0, f13 = 0.0;
+    if (__any_sync(0xffffffffu, (c0.z >= 0) | (c0.w >= 0) | (c1.z >= 0) | (c1.w >= 0))) {   // rare: > 2 far in a row
+      if (c0.z >= 0) f02 = pn_blk(dyns, stat, c0.z, c.a, c.b);
+      if (c0.w >= 0) f03 = pn_blk(dyns, stat, c0.w, c.a, c.b);
+      if (c1.z >= 0) f12 = pn_blk(dyns, stat, c1.z, c.a, c.b);
+      if (c1.w >= 0) f13 = pn_blk(dyns, stat, c1.w, c.a, c.b);
+    }
+    double s0 = p0 - nbv(c0.x, f00, p0);
+    s0 += p0 - nbv(c0.y, f01, p0);
+    s0 += p0 - nbv(c0.z, f02, p0);
+    s0 += p0 - nbv(c0.w, f03, p0);
+    double s1 = p1 - nbv(c1.x, f10, p1);
+    s1 += p1 - nbv(c1.y, f11, p1);
+    s1 += p1 - nbv(c1.z, f12, p1);
+    s1 += p1 - nbv(c1.w, f13, p1);
+    const double q0 = __fma_rn(C.Tconst, s0, __dmul_rn(ds.x, p0));
+    const double q1 = __fma_rn(C.Tconst, s1, __dmul_rn(ds.y, p1));
+    const int base = 64 * m + 2 * lane;
+    double* dd = dynd + (int64_t)m * kBDyn + 2 * lane;
+    // rows past n in the last chunk: their block slots exist (padded), the state vector's do not
+    st2mut(dd, make_double2(r0, r1n));
+    st2mut(dd + 64, make_double2(q0, q1));
+    st2mut(dd + 128, make_double2(p0, p1));
+    const double2 xn = make_double2(__fma_rn(c.a, po.x, xo.x), __fma_rn(c.a, po.y, xo.y));
+    if (base + 1 < r1) {
+      *reinterpret_cast<double2*>(xg + base) = xn;
+      c.accum(acc, p0, r0, di.x, q0);
+      c.accum(acc, p1, r1n, di.y, q1);
+    } else if (base < r1) {
+      xg[base] = xn.x;
+      c.accum(acc, p0, r0, di.x, q0);
     }
   }
 }
@@ -1124,11 +1074,11 @@ __device__ void iter_graph8(const Ctx& c, const ContDev& C, int r0, int r1,
 
 // ---------------------------------------------------------------- init pass
 // b = (m/tau) u + F + [D: sum sigma u_other];  r0 = b - K u;  x = u;  p0 = q0 = 0
-// recw: nullptr, or this row's 32-byte record {r, q, p, D^-1} of the streaming ELL pass
+// bw: nullptr, or this row's r slot in the chunk-blocked workspace (q, p follow 64 and 128 doubles on)
 template <bool CPL>
 __device__ __forceinline__ void init_row(const StepParams& P, int64_t gi, double Ku_nb,
                                          const double* uo, double* x, int myphase, double (&acc)[3],
-                                         double* recw = nullptr) {
+                                         double* bw = nullptr) {
   const double u = uo[gi];
   double b = ldro(P.mtau + gi) * u + ldro(P.F + gi);
   double Ku = ldro((CPL ? P.dsC : P.dsD) + gi) * u + Ku_nb;
@@ -1154,8 +1104,10 @@ __device__ __forceinline__ void init_row(const StepParams& P, int64_t gi, double
   const double r = b - Ku;
   const double di = ldro(P.dinv + gi);
   x[gi] = u;
-  if (recw) {
-    st_rec(recw, r, 0.0, 0.0, di);
+  if (bw) {
+    stmut(bw, r);
+    stmut(bw + 64, 0.0);
+    stmut(bw + 128, 0.0);
   } else {
     stmut(P.r[0] + gi, r);
     stmut(P.p[0] + gi, 0.0);
@@ -1196,7 +1148,7 @@ __device__ void init_item(const StepParams& P, const Item& it, const double* uo,
         const double t = C.val ? ldro(C.val + e) : C.Tconst;
         s += t * (u - uo[ldro(C.col + e)]);
       }
-      init_row<CPL>(P, gi, s, uo, x, myphase, acc, (!CPL && C.rec[0]) ? C.rec[0] + 4 * (int64_t)i : nullptr);
+      init_row<CPL>(P, gi, s, uo, x, myphase, acc, (!CPL && C.bstat) ? C.bdyn[0] + (int64_t)(i >> 6) * kBDyn + (i & 63) : nullptr);
     }
   }
 }
@@ -1922,7 +1874,7 @@ __device__ void run_group(const StepParams& P, int g, int cl, double* x, const d
       for (int k = 0; k < P.L; ++k)
         if (((G.cont_mask >> k) & 1) && P.cont[k].rr) {
           if (P.cont[k].resident) iter_ells_res<CPL>(c, P.cont[k], wg, W, st, j == 0, a5);
-          else if (!CPL && P.cont[k].rec[0]) iter_ells4(c, P.cont[k], wg, W, st, s, a5);
+          else if (!CPL && P.cont[k].bstat) iter_ellb(c, P.cont[k], wg, W, st, s, a5);
           else iter_ells<CPL>(c, P.cont[k], wg, W, st, a5);
         }
       for (int it = ib + wg; it < ie; it += W) {
