@@ -86,12 +86,12 @@ struct Ctx {
   double a, b;
 
   __device__ __forceinline__ double pn_at(int64_t gi) const {
-    MC_ASSERT(gi >= 0 && gi < P->N);
+    MC_ASSERT(gi >= 0 && gi < P->N + kSlack);   // rows past n of a last chunk read the zeroed slack, discarded
     return pnew(ldnb(rs + gi), ldnb(qs + gi), ldnb(ps + gi), ldro(P->dinv + gi), a, b);
   }
   // owner update of row gi: x, r, p stored; returns p_j, r_j, D^{-1}_ii
   __device__ __forceinline__ void own(int64_t gi, double& pn, double& rn, double& di) const {
-    MC_ASSERT(gi >= 0 && gi < P->N);
+    MC_ASSERT(gi >= 0 && gi < P->N + kSlack);   // rows past n of a last chunk read the zeroed slack, discarded
     const double ro = ldmut(rs + gi), qo = ldmut(qs + gi), po = ldmut(ps + gi);
     di = ldro(P->dinv + gi);
     const double xo = x[gi];
@@ -1204,23 +1204,28 @@ __device__ __forceinline__ void group_allreduce(const StepParams& P, int g, int 
   __syncthreads();
   double* part = P.partials + (size_t)(epoch & 1ull) * kNPart * P.total_ctas;
   PROF_T(ta);
-  if (threadIdx.x == 0) {
-#pragma unroll
-    for (int k = 0; k < NP; ++k) {
+  if (w == 0) {
+    if (lane < NP) {                                   // lane k: CTA partial of value k, fixed order
       double s = 0.0;
 #pragma unroll
-      for (int i = 0; i < kWarps; ++i) s += sh[eb][i][k];
-      __stcg(part + (size_t)k * P.total_ctas + base + cl, s);
+      for (int i = 0; i < kWarps; ++i) s += sh[eb][i][lane];
+      __stcg(part + (size_t)lane * P.total_ctas + base + cl, s);
     }
+    __syncwarp();
     // release: this CTA's r/p/q stores (ordered before by bar.sync) and its partials
-    unsigned long long* ctr = &P.sync->arrive[g * kCtrStride];
-    red_release_add(ctr, 1ull);
+    if (lane == 0) red_release_add(&P.sync->arrive[(g * kNSub + cl % kNSub) * kCtrStride], 1ull);
     PROF_T(tb);
-    const unsigned long long target = (epoch + 1ull) * (unsigned long long)G;
-    while (ld_acquire(ctr) < target) {
+    // lane s polls sub-counter s: the CTAs cl = s, s + kNSub, ... of the group arrive there
+    if (lane < kNSub) {
+      const unsigned long long cnt = (unsigned long long)((G - lane + kNSub - 1) / kNSub);
+      const unsigned long long target = (epoch + 1ull) * cnt;
+      const unsigned long long* ctr = &P.sync->arrive[(g * kNSub + lane) * kCtrStride];
+      while (ld_acquire(ctr) < target) {
+      }
     }
+    __syncwarp();
 #if MC_PROF
-    if (cl == 0) {
+    if (cl == 0 && lane == 0) {
       PROF_T(tc);
       PROF_ADD(g, 1, tb - ta);
       PROF_ADD(g, 2, tc - tb);
