@@ -1292,6 +1292,8 @@ static mc_status enqueue_step(mc_ctx* c, int scheme, mc_step_report* rep_dev, cu
         P.cont[a].bjs = (!P.cont[a].bj && nconts == 1 && c->tinv[a] != nullptr && scheme != MC_COUPLED) ? 1 : 0;
         // streaming Jacobi pass of a decoupled solve: chunk-blocked workspace (the CG-state
         // blocks are allocated the first time a plan streams this network)
+        if (use_blocked() && c->bstat[a] && nconts == 1 && scheme != MC_COUPLED && P.cont[a].resident)
+          P.cont[a].bstat = c->bstat[a];          // resident pass on the blocked static data
         if (use_blocked() && c->bstat[a] && nconts == 1 && scheme != MC_COUPLED && !P.cont[a].resident &&
             !P.cont[a].bj && !P.cont[a].bjs) {
           if (!c->bdyn[a][0]) {

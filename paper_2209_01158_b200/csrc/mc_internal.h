@@ -38,11 +38,12 @@ constexpr int kNPart = 5;              // reduction slots per barrier (pq, rr, r
 constexpr int kPadDofs = 32;           // continuum offsets padded to 32 doubles (256 B)
 constexpr int kCtrStride = 32;         // barrier counters 256 B apart (own L2 line / slice)
 #ifndef MC_NSUB
-#define MC_NSUB 8
+#define MC_NSUB 1
 #endif
-constexpr int kNSub = MC_NSUB;         // arrival sub-counters per group barrier: CTA cl arrives on counter
-                                       // cl % kNSub, lanes 0..kNSub-1 of warp 0 poll one each -- the
-                                       // arrivals of ~150 CTAs no longer serialise on one L2 address
+constexpr int kNSub = MC_NSUB;         // arrival sub-counters per group barrier (CTA cl arrives on counter
+                                       // cl % kNSub, lanes 0..kNSub-1 of warp 0 poll one each).  Measured
+                                       // with 8: no gain (config-1 fracture 5.4 vs 5.3 us per iteration,
+                                       // profiles/r02_barrier_subcounters.txt), so the default is one
 constexpr int kSlack = 128;            // extra doubles after every per-DOF array (staged over-reads)
 // cp.async staging: per warp, two slots of the next rows' operands
 constexpr int kSlotG = 536;            // grid strip slot: 8 arrays x 64 doubles + 18 edge doubles

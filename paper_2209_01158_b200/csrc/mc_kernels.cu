@@ -945,6 +945,107 @@ __device__ void iter_ells_res(const Ctx& c, const ContDev& C, int wg, int W, con
   }
 }
 
+// Resident pass on the chunk-blocked static data (decoupled solves; same arithmetic as
+// iter_ells_res with a third of its instructions): the slot holds the chunk's bstat block
+// (D^-1, shift, far-first int32 codes [64][4]) and r, q, p, x (64 doubles each) for the
+// whole solve; far neighbours (slots 0 and 1 of a row; rarely 2 and 3) are gathered from
+// the previous iteration's r, q, p in global memory, in-chunk neighbours read the new p
+// from the slot.  r, p, q are published to global every iteration; x at the end.
+__device__ void iter_ells_res2(const Ctx& c, const ContDev& C, int wg, int W, const Stage& st, bool first,
+                               double (&acc)[kNPart]) {
+  double* wsm = st.wsm;
+  const int lane = threadIdx.x & 31;
+  const int64_t off = C.off;
+  const int r1 = (int)C.n;
+  const int nch = (r1 + 63) / 64;
+  if (first) {
+    for (int m = wg, t = 0; m < nch; m += W, ++t) {
+      double* sl = wsm + t * kSlotE;
+      __syncwarp();
+      if (lane == 0) {
+        const int64_t g = off + 64 * (int64_t)m;
+        st.begin(t, 8u * kBStat + 4u * 512u);
+        uint64_t* bar = st.bars + t;
+        bulk_g2s(sl, C.bstat + (int64_t)m * kBStat, 8u * kBStat, bar);
+        bulk_g2s(sl + 256, c.rs + g, 512, bar);
+        bulk_g2s(sl + 320, c.qs + g, 512, bar);
+        bulk_g2s(sl + 384, c.ps + g, 512, bar);
+        bulk_g2s(sl + 448, c.x + g, 512, bar);
+      }
+    }
+    for (int m = wg, t = 0; m < nch; m += W, ++t) st.wait(t);
+  }
+  for (int m = wg, t = 0; m < nch; m += W, ++t) {
+    double* sl = wsm + t * kSlotE;
+    const int base = 64 * m + 2 * lane;
+    const int64_t g = off + base;
+    const int4 c0 = *reinterpret_cast<const int4*>(sl + 128 + 4 * lane);
+    const int4 c1 = *reinterpret_cast<const int4*>(sl + 128 + 4 * lane + 2);
+    double f00 = 0.0, f01 = 0.0, f10 = 0.0, f11 = 0.0;
+    if (c0.x >= 0) f00 = c.pn_at(off + c0.x);
+    if (c0.y >= 0) f01 = c.pn_at(off + c0.y);
+    if (c1.x >= 0) f10 = c.pn_at(off + c1.x);
+    if (c1.y >= 0) f11 = c.pn_at(off + c1.y);
+    const double2 di = *reinterpret_cast<const double2*>(sl + 2 * lane);
+    const double2 ds = *reinterpret_cast<const double2*>(sl + 64 + 2 * lane);
+    const double2 ro = *reinterpret_cast<const double2*>(sl + 256 + 2 * lane);
+    const double2 qo = *reinterpret_cast<const double2*>(sl + 320 + 2 * lane);
+    const double2 po = *reinterpret_cast<const double2*>(sl + 384 + 2 * lane);
+    const double2 xo = *reinterpret_cast<const double2*>(sl + 448 + 2 * lane);
+    const double r0 = __fma_rn(-c.a, qo.x, ro.x), r1n = __fma_rn(-c.a, qo.y, ro.y);
+    const double p0 = __fma_rn(di.x, r0, __dmul_rn(c.b, po.x)), p1 = __fma_rn(di.y, r1n, __dmul_rn(c.b, po.y));
+    *reinterpret_cast<double2*>(sl + 448 + 2 * lane) = make_double2(__fma_rn(c.a, po.x, xo.x), __fma_rn(c.a, po.y, xo.y));
+    *reinterpret_cast<double2*>(sl + 256 + 2 * lane) = make_double2(r0, r1n);
+    __syncwarp();                                                 // every lane has read the old p
+    *reinterpret_cast<double2*>(sl + 384 + 2 * lane) = make_double2(p0, p1);
+    const bool ok0 = base < r1, ok1 = base + 1 < r1;
+    if (ok1) {
+      st2mut(c.rd + g, make_double2(r0, r1n));
+      st2mut(c.pd + g, make_double2(p0, p1));
+    } else if (ok0) {
+      stmut(c.rd + g, r0);
+      stmut(c.pd + g, p0);
+    }
+    __syncwarp();
+    const double* pn = sl + 384;
+    auto nbv = [&](int32_t cd, double far, double own) { return cd >= 0 ? far : (cd <= -2 ? pn[-2 - cd] : own); };
+    double f02 = 0.0, f03 = 0.0, f12 = 0.0, f13 = 0.0;
+    if (__any_sync(0xffffffffu, (c0.z >= 0) | (c0.w >= 0) | (c1.z >= 0) | (c1.w >= 0))) {   // rare: > 2 far in a row
+      if (c0.z >= 0) f02 = c.pn_at(off + c0.z);
+      if (c0.w >= 0) f03 = c.pn_at(off + c0.w);
+      if (c1.z >= 0) f12 = c.pn_at(off + c1.z);
+      if (c1.w >= 0) f13 = c.pn_at(off + c1.w);
+    }
+    double s0 = p0 - nbv(c0.x, f00, p0);
+    s0 += p0 - nbv(c0.y, f01, p0);
+    s0 += p0 - nbv(c0.z, f02, p0);
+    s0 += p0 - nbv(c0.w, f03, p0);
+    double s1 = p1 - nbv(c1.x, f10, p1);
+    s1 += p1 - nbv(c1.y, f11, p1);
+    s1 += p1 - nbv(c1.z, f12, p1);
+    s1 += p1 - nbv(c1.w, f13, p1);
+    const double q0 = __fma_rn(C.Tconst, s0, __dmul_rn(ds.x, p0));
+    const double q1 = __fma_rn(C.Tconst, s1, __dmul_rn(ds.y, p1));
+    *reinterpret_cast<double2*>(sl + 320 + 2 * lane) = make_double2(q0, q1);
+    if (ok1) st2mut(c.qd + g, make_double2(q0, q1));
+    else if (ok0) stmut(c.qd + g, q0);
+    if (ok0) c.accum(acc, p0, r0, di.x, q0);
+    if (ok1) c.accum(acc, p1, r1n, di.y, q1);
+  }
+}
+
+__device__ void flush_ells_res2(const ContDev& C, int wg, int W, const double* wsm, double* x) {
+  const int lane = threadIdx.x & 31;
+  const int nch = (int)((C.n + 63) / 64);
+  for (int m = wg, t = 0; m < nch; m += W, ++t) {
+    const double* sl = wsm + t * kSlotE;
+    for (int h = 0; h < 2; ++h) {
+      const int64_t i = 64 * (int64_t)m + 2 * lane + h;
+      if (i < C.n) x[C.off + i] = sl[448 + 2 * lane + h];
+    }
+  }
+}
+
 __device__ void flush_ells_res(const ContDev& C, int wg, int W, const double* wsm, double* x) {
   const int lane = threadIdx.x & 31;
   const int nch = (int)((C.n + 63) / 64);
@@ -1148,7 +1249,7 @@ __device__ void init_item(const StepParams& P, const Item& it, const double* uo,
         const double t = C.val ? ldro(C.val + e) : C.Tconst;
         s += t * (u - uo[ldro(C.col + e)]);
       }
-      init_row<CPL>(P, gi, s, uo, x, myphase, acc, (!CPL && C.bstat) ? C.bdyn[0] + (int64_t)(i >> 6) * kBDyn + (i & 63) : nullptr);
+      init_row<CPL>(P, gi, s, uo, x, myphase, acc, (!CPL && C.bdyn[0]) ? C.bdyn[0] + (int64_t)(i >> 6) * kBDyn + (i & 63) : nullptr);
     }
   }
 }
@@ -1878,8 +1979,10 @@ __device__ void run_group(const StepParams& P, int g, int cl, double* x, const d
       PROF_T(tp0);
       for (int k = 0; k < P.L; ++k)
         if (((G.cont_mask >> k) & 1) && P.cont[k].rr) {
-          if (P.cont[k].resident) iter_ells_res<CPL>(c, P.cont[k], wg, W, st, j == 0, a5);
-          else if (!CPL && P.cont[k].bstat) iter_ellb(c, P.cont[k], wg, W, st, s, a5);
+          if (P.cont[k].resident) {
+            if (!CPL && P.cont[k].bstat) iter_ells_res2(c, P.cont[k], wg, W, st, j == 0, a5);
+            else iter_ells_res<CPL>(c, P.cont[k], wg, W, st, j == 0, a5);
+          } else if (!CPL && P.cont[k].bdyn[0]) iter_ellb(c, P.cont[k], wg, W, st, s, a5);
           else iter_ells<CPL>(c, P.cont[k], wg, W, st, a5);
         }
       for (int it = ib + wg; it < ie; it += W) {
@@ -1928,7 +2031,10 @@ __device__ void run_group(const StepParams& P, int g, int cl, double* x, const d
   }
   if (passes > 0)
     for (int k = 0; k < P.L; ++k)
-      if (((G.cont_mask >> k) & 1) && P.cont[k].rr && P.cont[k].resident) flush_ells_res(P.cont[k], wg, W, wsm, x);
+      if (((G.cont_mask >> k) & 1) && P.cont[k].rr && P.cont[k].resident) {
+        if (!CPL && P.cont[k].bstat) flush_ells_res2(P.cont[k], wg, W, wsm, x);
+        else flush_ells_res(P.cont[k], wg, W, wsm, x);
+      }
   if (zero)
     for (int it = ib + wg; it < ie; it += W) zero_item(P, P.items[it], x);
   if (zero)
