@@ -59,6 +59,8 @@ struct HostCont {
   int64_t estride = 0;                         // graph: ELL stride
   bool bj = false;                             // graph: block-Jacobi preconditioner (mc_set_preconditioner)
   std::vector<int32_t> perm, inv;              // graph: internal position -> caller index, inverse
+  int maxdeg = 0;                              // graph: largest neighbour count
+  bool anyfixed = false;                       // graph: has fixed (Dirichlet) cells
   std::vector<uint8_t> fixed;                  // graph Dirichlet DOFs
   std::vector<double> gfix;
 };
@@ -105,6 +107,7 @@ struct mc_ctx {
   int32_t* ecol[MC_MAX_CONTINUA] = {nullptr};
   int32_t* perm[MC_MAX_CONTINUA] = {nullptr};   // graph: internal -> caller numbering
   double* bstat[MC_MAX_CONTINUA] = {nullptr};                // chunk-blocked streaming ELL pass: static blocks
+  double* bstat16[MC_MAX_CONTINUA] = {nullptr};              //   compact static blocks (uint16 codes, D^-1 recomputed)
   double* bdyn[MC_MAX_CONTINUA][2] = {{nullptr, nullptr}};   //   and CG-state blocks (allocated on first use)
   double* tinv[MC_MAX_CONTINUA] = {nullptr};    // bj: chunk Thomas factors
   double* tcp[MC_MAX_CONTINUA] = {nullptr};
@@ -729,6 +732,8 @@ extern "C" mc_status mc_set_continuum(mc_ctx* c, int32_t alpha, const mc_continu
     int maxdeg = 0;
     for (int64_t i = 0; i < H.n; ++i) maxdeg = std::max(maxdeg, H.rowptr[(size_t)i + 1] - H.rowptr[(size_t)i]);
     const char* ch = getenv("MC_CHAIN");
+    H.maxdeg = maxdeg;
+    H.anyfixed = std::any_of(H.fixed.begin(), H.fixed.end(), [](uint8_t f) { return f != 0; });
     H.bj = (c->precond == MC_PRECOND_BLOCK) && maxdeg <= 4 && H.val.empty();
     if (maxdeg <= 4 && ((ch && ch[0] == '1') || H.bj)) apply_chain_order(H);
   }
@@ -859,7 +864,13 @@ static mc_status finalize(mc_ctx* c) {
     for (int64_t i = 0; i < c->hc[a].n; ++i) {
       const size_t g = (size_t)(c->off[a] + i);
       dsD[g] = dbase[g] + sig[g];
-      const double diag = dsD[g] + tsum[g];            // diag(K), Jacobi (reading C14)
+      // diag(K), Jacobi (reading C14).  A network with one transmissibility T and <= 4
+      // neighbours per row: ds + T deg in one rounding -- the streaming pass recomputes
+      // exactly this from ds and the neighbour count (iter_ellb16)
+      const HostCont& Hc = c->hc[a];
+      const bool ellu = Hc.kind == KIND_GRAPH && Hc.val.empty() && Hc.maxdeg <= 4 && !Hc.bj && !Hc.anyfixed;
+      const double diag = ellu ? std::fma(Hc.Tconst, (double)(Hc.rowptr[(size_t)i + 1] - Hc.rowptr[(size_t)i]), dsD[g])
+                               : dsD[g] + tsum[g];
       if (!(diag > 0.0) || !std::isfinite(diag))
         return fail(c, MC_ERR_ARG, "continuum %d row %lld: diagonal %g of M/tau + A is not > 0", a,
                     (long long)i, diag);
@@ -929,6 +940,34 @@ static mc_status finalize(mc_ctx* c) {
               }
           }
           UP(c->bstat[a], bst);
+          // compact blocks (iter_ellb16): shift (64) | uint16 codes [64][4]; only when every
+          // neighbour lies within 127 chunks of its row
+          std::vector<double> b16((size_t)nchk * kBStat16, 0.0);
+          bool fits = true;
+          for (int64_t m = 0; m < nchk; ++m) {
+            uint16_t* cp = reinterpret_cast<uint16_t*>(&b16[(size_t)(m * kBStat16 + 64)]);
+            for (int q = 0; q < 256; ++q) cp[q] = 0xFFFFu;
+          }
+          for (int64_t i = 0; i < H.n && fits; ++i) {
+            const int64_t m = i >> 6, w = i & 63;
+            b16[(size_t)(m * kBStat16 + w)] = dsD[(size_t)(c->off[a] + i)];
+            uint16_t* cp = reinterpret_cast<uint16_t*>(&b16[(size_t)(m * kBStat16 + 64)]) + 4 * w;
+            int k = 0;
+            for (int pass = 0; pass < 2; ++pass)                 // far neighbours first
+              for (int32_t e = H.rowptr[(size_t)i]; e < H.rowptr[(size_t)i + 1]; ++e) {
+                const int64_t j = H.col[(size_t)e];
+                const int64_t dch = (j >> 6) - m;
+                const bool far = dch != 0;
+                if (far != (pass == 0)) continue;
+                if (dch < -127 || dch > 127) {
+                  fits = false;
+                  break;
+                }
+                const int degj = H.rowptr[(size_t)j + 1] - H.rowptr[(size_t)j];
+                cp[k++] = (uint16_t)(((dch + 127) << 8) | ((degj - 1) << 6) | (j & 63));
+              }
+          }
+          if (fits && !H.anyfixed) UP(c->bstat16[a], b16);
         }
         if (H.bj) {
           // block-Jacobi: tridiagonal part of every 64-row chunk (rows i, i+1 of the
@@ -1073,6 +1112,15 @@ static int64_t one_cta_work() {
 static bool use_blocked() {
   static const bool v = [] {
     const char* e = getenv("MC_BLOCKED");
+    return !(e && e[0] == '0');
+  }();
+  return v;
+}
+
+// MC_COMPACT=0 (dev, A/B): 96-byte blocked pass (int32 codes, stored D^-1) instead of the 80-byte one
+static bool use_compact() {
+  static const bool v = [] {
+    const char* e = getenv("MC_COMPACT");
     return !(e && e[0] == '0');
   }();
   return v;
@@ -1305,6 +1353,7 @@ static mc_status enqueue_step(mc_ctx* c, int scheme, mc_step_report* rep_dev, cu
             }
           }
           P.cont[a].bstat = c->bstat[a];
+          P.cont[a].bstat16 = use_compact() ? c->bstat16[a] : nullptr;
           P.cont[a].bdyn[0] = c->bdyn[a][0];
           P.cont[a].bdyn[1] = c->bdyn[a][1];
         }

@@ -50,6 +50,7 @@ constexpr int kSlotG = 536;            // grid strip slot: 8 arrays x 64 doubles
 constexpr int kSlotE = 528;            // ELL chunk slot: r, q, p, D^-1 windows (68), x, shift (64), 4 x 64 int32 codes
 constexpr int kStagesE = 2;                // ELL pass: chunk in flight + chunk computed
 constexpr int kBStat = 256;                // chunk-blocked pass: doubles of static data per chunk
+constexpr int kBStat16 = 128;              //   compact variant: shift (64) + uint16 codes [64][4] (64); D^-1 recomputed
 constexpr int kBDyn = 192;                 //                     doubles of CG state per chunk and parity
 constexpr int kPnBuf = 72;                 // ELL pass: new p of the chunk window (68) per warp
 #ifndef MC_BJS_STAGES
@@ -86,6 +87,7 @@ struct ContDev {
   int32_t bjs;             // block-Jacobi, streaming passes (network too large to stay resident)
   // chunk-blocked workspace of the streaming ELL pass of a decoupled Jacobi solve:
   const double* bstat;     // per 64-row chunk 256 doubles: D^-1 (64), shift (64), 4 int32 codes per row (128)
+  const double* bstat16;   // compact static blocks, 128 doubles per chunk: shift (64), 4 uint16 codes per row (64)
   double* bdyn[2];         // per chunk 192 doubles: r (64), q (64), p (64); double-buffered by iteration parity
   const double* tinv;      // bj: Thomas factors of each 64-row chunk's tridiagonal block:
   const double* tcp;       //     1 / pivot, super-diagonal multiplier c', sub-diagonal e_{i-1}

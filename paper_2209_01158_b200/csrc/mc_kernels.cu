@@ -793,6 +793,118 @@ __device__ void iter_ellb(const Ctx& c, const ContDev& C, int wg, int W, const S
   }
 }
 
+// Compact variant of iter_ellb (80 instead of 96 B per row and iteration): the static block
+// is 128 doubles -- the D-scheme shift ds (64) and four uint16 codes per row (64) -- and
+// D^-1 = 1 / (ds + T deg) is recomputed (the network has one transmissibility T, deg = the
+// row's neighbour count; finalize stores exactly this value in P.dinv, so owners, far
+// gatherers and the init pass all use the same bits).  Code u: 0xFFFF none; otherwise
+// w = u & 63 (row in its chunk), (u >> 6) & 3 = the NEIGHBOUR's deg - 1, (u >> 8) - 127 =
+// its chunk relative to this one (0: this chunk, read the new p from the warp's buffer).
+// Built by finalize when every neighbour lies within 127 chunks (else bstat / iter_ellb).
+__device__ __forceinline__ double dinv_deg(double ds, int deg, double T) {
+  return __drcp_rn(__fma_rn(T, (double)deg, ds));
+}
+__device__ __forceinline__ double pn_blk16(const double* dyn, const double* stat, int m, unsigned u, double T,
+                                           double a, double b) {
+  const int64_t blk = (int64_t)m + (int)(u >> 8) - 127;
+  const int w = u & 63;
+  const double* d = dyn + blk * kBDyn + w;
+  const double di = dinv_deg(ldro(stat + blk * kBStat16 + w), (int)((u >> 6) & 3) + 1, T);
+  return pnew(ldnb(d), ldnb(d + 64), ldnb(d + 128), di, a, b);
+}
+
+__device__ void iter_ellb16(const Ctx& c, const ContDev& C, int wg, int W, const Stage& st, int s,
+                            double (&acc)[kNPart]) {
+  double* wsm = st.wsm;
+  double* pnb = wsm + kWarpSmem - kPnBuf;                      // new p of the chunk's rows
+  const int lane = threadIdx.x & 31;
+  const int r1 = (int)C.n;
+  const int nch = (r1 + 63) / 64;
+  const double* stat = C.bstat16;
+  const double* dyns = C.bdyn[s];
+  double* dynd = C.bdyn[s ^ 1];
+  double* xg = c.x + C.off;
+  const double T = C.Tconst;
+  auto prefetch = [&](int m, int t) {
+    double* sl = wsm + t * kSlotE;
+    __syncwarp();
+    if (lane == 0) {
+      st.begin(t, 8u * (kBStat16 + kBDyn + 64));
+      uint64_t* bar = st.bars + t;
+      bulk_g2s(sl, stat + (int64_t)m * kBStat16, 8u * kBStat16, bar);
+      bulk_g2s(sl + kBStat16, dyns + (int64_t)m * kBDyn, 8u * kBDyn, bar);
+      bulk_g2s(sl + kBStat16 + kBDyn, xg + 64 * (int64_t)m, 512, bar);
+    }
+  };
+  if (wg >= nch) return;
+  prefetch(wg, 0);
+  int t = 0;
+  auto none = [](unsigned u) { return u == 0xFFFFu; };
+  auto isfar = [](unsigned u) { return u != 0xFFFFu && (u >> 8) != 127u; };
+  for (int m = wg; m < nch; m += W, t ^= 1) {
+    if (m + W < nch) prefetch(m + W, t ^ 1);                      // next chunk in flight
+    st.wait(t);
+    const double* sl = wsm + t * kSlotE;
+    // codes of rows 2 lane, 2 lane + 1: 8 consecutive uint16
+    const uint4 cw = *reinterpret_cast<const uint4*>(sl + 64 + 2 * lane);
+    const unsigned u00 = cw.x & 0xFFFFu, u01 = cw.x >> 16, u02 = cw.y & 0xFFFFu, u03 = cw.y >> 16;
+    const unsigned u10 = cw.z & 0xFFFFu, u11 = cw.z >> 16, u12 = cw.w & 0xFFFFu, u13 = cw.w >> 16;
+    // far neighbours (slots 0, 1 of each row): gathered in one batch, loads predicated per lane
+    double f00 = 0.0, f01 = 0.0, f10 = 0.0, f11 = 0.0;
+    if (isfar(u00)) f00 = pn_blk16(dyns, stat, m, u00, T, c.a, c.b);
+    if (isfar(u01)) f01 = pn_blk16(dyns, stat, m, u01, T, c.a, c.b);
+    if (isfar(u10)) f10 = pn_blk16(dyns, stat, m, u10, T, c.a, c.b);
+    if (isfar(u11)) f11 = pn_blk16(dyns, stat, m, u11, T, c.a, c.b);
+    const double2 ds = *reinterpret_cast<const double2*>(sl + 2 * lane);
+    const int deg0 = 4 - (int)none(u00) - (int)none(u01) - (int)none(u02) - (int)none(u03);
+    const int deg1 = 4 - (int)none(u10) - (int)none(u11) - (int)none(u12) - (int)none(u13);
+    const double di0 = dinv_deg(ds.x, deg0, T), di1 = dinv_deg(ds.y, deg1, T);
+    const double2 ro = *reinterpret_cast<const double2*>(sl + kBStat16 + 2 * lane);
+    const double2 qo = *reinterpret_cast<const double2*>(sl + kBStat16 + 64 + 2 * lane);
+    const double2 po = *reinterpret_cast<const double2*>(sl + kBStat16 + 128 + 2 * lane);
+    const double2 xo = *reinterpret_cast<const double2*>(sl + kBStat16 + kBDyn + 2 * lane);
+    const double r0 = __fma_rn(-c.a, qo.x, ro.x), r1n = __fma_rn(-c.a, qo.y, ro.y);
+    const double p0 = __fma_rn(di0, r0, __dmul_rn(c.b, po.x)), p1 = __fma_rn(di1, r1n, __dmul_rn(c.b, po.y));
+    __syncwarp();                                                 // previous chunk's pnb reads done
+    *reinterpret_cast<double2*>(pnb + 2 * lane) = make_double2(p0, p1);
+    __syncwarp();
+    auto nbv = [&](unsigned u, double far, double own) {
+      return none(u) ? own : ((u >> 8) == 127u ? pnb[u & 63u] : far);
+    };
+    double f02 = 0.0, f03 = 0.0, f12 = 0.0, f13 = 0.0;
+    if (__any_sync(0xffffffffu, isfar(u02) | isfar(u03) | isfar(u12) | isfar(u13))) {   // rare: > 2 far in a row
+      if (isfar(u02)) f02 = pn_blk16(dyns, stat, m, u02, T, c.a, c.b);
+      if (isfar(u03)) f03 = pn_blk16(dyns, stat, m, u03, T, c.a, c.b);
+      if (isfar(u12)) f12 = pn_blk16(dyns, stat, m, u12, T, c.a, c.b);
+      if (isfar(u13)) f13 = pn_blk16(dyns, stat, m, u13, T, c.a, c.b);
+    }
+    double s0 = p0 - nbv(u00, f00, p0);
+    s0 += p0 - nbv(u01, f01, p0);
+    s0 += p0 - nbv(u02, f02, p0);
+    s0 += p0 - nbv(u03, f03, p0);
+    double s1 = p1 - nbv(u10, f10, p1);
+    s1 += p1 - nbv(u11, f11, p1);
+    s1 += p1 - nbv(u12, f12, p1);
+    s1 += p1 - nbv(u13, f13, p1);
+    const double q0 = __fma_rn(T, s0, __dmul_rn(ds.x, p0));
+    const double q1 = __fma_rn(T, s1, __dmul_rn(ds.y, p1));
+    const int base = 64 * m + 2 * lane;
+    double* dd = dynd + (int64_t)m * kBDyn + 2 * lane;
+    st2mut(dd, make_double2(r0, r1n));
+    st2mut(dd + 64, make_double2(q0, q1));
+    st2mut(dd + 128, make_double2(p0, p1));
+    const double2 xn = make_double2(__fma_rn(c.a, po.x, xo.x), __fma_rn(c.a, po.y, xo.y));
+    if (base + 1 < r1) {
+      *reinterpret_cast<double2*>(xg + base) = xn;
+      c.accum(acc, p0, r0, di0, q0);
+      c.accum(acc, p1, r1n, di1, q1);
+    } else if (base < r1) {
+      xg[base] = xn.x;
+      c.accum(acc, p0, r0, di0, q0);
+    }
+  }
+}
+
 // Resident variant for latency-bound graphs (every warp owns <= kStages chunks,
 // DESIGN.md §5.3): the chunks' r, q, p, x, D^-1, shift and codes stay in this warp's
 // slots for the whole solve, so an iteration streams nothing; in-chunk neighbours read
@@ -1982,7 +2094,10 @@ __device__ void run_group(const StepParams& P, int g, int cl, double* x, const d
           if (P.cont[k].resident) {
             if (!CPL && P.cont[k].bstat) iter_ells_res2(c, P.cont[k], wg, W, st, j == 0, a5);
             else iter_ells_res<CPL>(c, P.cont[k], wg, W, st, j == 0, a5);
-          } else if (!CPL && P.cont[k].bdyn[0]) iter_ellb(c, P.cont[k], wg, W, st, s, a5);
+          } else if (!CPL && P.cont[k].bdyn[0]) {
+            if (P.cont[k].bstat16) iter_ellb16(c, P.cont[k], wg, W, st, s, a5);
+            else iter_ellb(c, P.cont[k], wg, W, st, s, a5);
+          }
           else iter_ells<CPL>(c, P.cont[k], wg, W, st, a5);
         }
       for (int it = ib + wg; it < ie; it += W) {
