@@ -104,3 +104,41 @@ def test_block_jacobi_streaming_parity(kind, scheme, ctas):
                 worst = max(worst, np.linalg.norm(g[n][a] - r) / np.linalg.norm(r))
         assert worst <= 1e-9, worst
     assert its[1:, -1].sum() < its_j[1:, -1].sum()
+
+
+def test_block_jacobi_streaming_three_stage_build():
+    """The MC_BJS_STAGES=3 build (a third staging slot per warp in the streaming block-Jacobi
+    passes: `% kStagesB` slot indexing, mbarrier parity flips on slot reuse) against the
+    oracle at 1e-9, one CTA (8 warps for 42 chunks: every slot is refilled).  Runs in a fresh
+    process because the library is chosen at load time (MC_LIB)."""
+    import os
+    import subprocess
+    import sys
+    from paper_2209_01158_b200 import build
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    lib = os.path.join(root, "paper_2209_01158_b200", "libmc_bjs3.so")
+    srcs = [os.path.join(build.CSRC, f) for f in os.listdir(build.CSRC)]
+    if not os.path.exists(lib) or any(os.path.getmtime(f) > os.path.getmtime(lib) for f in srcs):
+        build.build(force=True, defines=["MC_BJS_STAGES=3"], out=lib)
+    code = (
+        "import sys, numpy as np\n"
+        f"sys.path.insert(0, {root!r})\n"
+        "from inputs import make_paper_analogue\n"
+        "from oracle import assemble as asm, schemes\n"
+        "from paper_2209_01158_b200 import Problem, permeability_order\n"
+        "scn = make_paper_analogue('2C')\n"
+        "sys_ = asm.assemble(scn)\n"
+        "ref = schemes.run(sys_, 'D', scn['T'] / scn['NT'], 6, order_by_k=permeability_order(scn))\n"
+        "pb = Problem(scn, precond='block', ctas=1)\n"
+        "worst = 0.0\n"
+        "for n in range(6):\n"
+        "    rep = pb.step('D')\n"
+        "    assert rep['paths'][1] == 4, rep['paths']\n"
+        "    got = [t.cpu().numpy() for t in pb.state()]\n"
+        "    for a, r in enumerate(sys_.split(ref[n])):\n"
+        "        worst = max(worst, np.linalg.norm(got[a] - r) / np.linalg.norm(r))\n"
+        "print('worst', worst)\n"
+        "assert worst <= 1e-9, worst\n")
+    r = subprocess.run([sys.executable, "-c", code], env=dict(os.environ, MC_LIB=lib), capture_output=True,
+                       text=True, timeout=900)
+    assert r.returncode == 0, r.stdout[-1500:] + r.stderr[-1500:]
