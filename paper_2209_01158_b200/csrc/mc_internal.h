@@ -58,9 +58,15 @@ constexpr int kPnBuf = 72;                 // ELL pass: new p of the chunk windo
 #endif
 constexpr int kStagesB = MC_BJS_STAGES;    // streaming block-Jacobi passes: chunks in flight + 1
 constexpr int kStagesEB = (kStagesE > kStagesB) ? kStagesE : kStagesB;
-constexpr int kWarpSmem = ((kStages * kSlotG > kStagesEB * kSlotE) ? kStages * kSlotG : kStagesEB * kSlotE) + kPnBuf;
+#ifndef MC_STAGES_C
+#define MC_STAGES_C 3
+#endif
+constexpr int kStagesC = MC_STAGES_C;      // compact blocked pass (iter_ellb16): chunks in flight + 1
+constexpr int kSlotC = 384;                // its slot: 128 static + 192 CG state + 64 x
+constexpr int kMaxI(int a, int b) { return a > b ? a : b; }
+constexpr int kWarpSmem = kMaxI(kMaxI(kStages * kSlotG, kStagesEB * kSlotE), kStagesC * kSlotC) + kPnBuf;
 // bytes per CTA: staging slots, then one mbarrier per slot per warp, then a parity word per warp
-constexpr int kNBars = (kStages > kStagesEB) ? kStages : kStagesEB;   // mbarriers per warp
+constexpr int kNBars = kMaxI(kMaxI(kStages, kStagesEB), kStagesC);   // mbarriers per warp
 constexpr int kDynSmem = kWarps * kWarpSmem * 8 + kWarps * kNBars * 8 + kWarps * 8;
 
 enum ContKind : int32_t { KIND_GRID = 0, KIND_GRAPH = 1 };

@@ -826,7 +826,7 @@ __device__ void iter_ellb16(const Ctx& c, const ContDev& C, int wg, int W, const
   double* xg = c.x + C.off;
   const double T = C.Tconst;
   auto prefetch = [&](int m, int t) {
-    double* sl = wsm + t * kSlotE;
+    double* sl = wsm + t * kSlotC;
     __syncwarp();
     if (lane == 0) {
       st.begin(t, 8u * (kBStat16 + kBDyn + 64));
@@ -837,14 +837,19 @@ __device__ void iter_ellb16(const Ctx& c, const ContDev& C, int wg, int W, const
     }
   };
   if (wg >= nch) return;
-  prefetch(wg, 0);
+#pragma unroll
+  for (int d = 0; d < kStagesC - 1; ++d)
+    if (wg + d * W < nch) prefetch(wg + d * W, d);                // kStagesC - 1 chunks in flight
   int t = 0;
   auto none = [](unsigned u) { return u == 0xFFFFu; };
   auto isfar = [](unsigned u) { return u != 0xFFFFu && (u >> 8) != 127u; };
-  for (int m = wg; m < nch; m += W, t ^= 1) {
-    if (m + W < nch) prefetch(m + W, t ^ 1);                      // next chunk in flight
+  for (int m = wg; m < nch; m += W, t = (t + 1 == kStagesC ? 0 : t + 1)) {
+    {
+      const int tn = t + kStagesC - 1 >= kStagesC ? t - 1 : t + kStagesC - 1;   // slot freed by the previous chunk
+      if (m + (kStagesC - 1) * W < nch) prefetch(m + (kStagesC - 1) * W, tn);
+    }
     st.wait(t);
-    const double* sl = wsm + t * kSlotE;
+    const double* sl = wsm + t * kSlotC;
     // codes of rows 2 lane, 2 lane + 1: 8 consecutive uint16
     const uint4 cw = *reinterpret_cast<const uint4*>(sl + 64 + 2 * lane);
     const unsigned u00 = cw.x & 0xFFFFu, u01 = cw.x >> 16, u02 = cw.y & 0xFFFFu, u03 = cw.y >> 16;
