@@ -39,6 +39,18 @@ def cpu_model():
     return "unknown"
 
 
+def load_coupled(args, lean, rec, check, tlast, cur_iters):
+    """Coupled scheme against whole-state files of a --save run (config 2: 71.5 MB per step)."""
+    meta = json.load(open(os.path.join(args.load, f"config{args.config}_coupled.json")))
+    rec["oracle"]["precomputed"] = dict(meta["oracle"], what="every step, whole state")
+    rec["oracle_iters_precomputed"] = [r["oracle_iters"] for r in meta["steps"]]
+    for n in range(1, args.steps + 1):
+        u = np.load(os.path.join(args.load, f"config{args.config}_coupled_step{n}.npy"))
+        tlast[0] = time.perf_counter() - meta["steps"][n - 1]["oracle_s"]
+        cur_iters[:] = meta["steps"][n - 1]["oracle_iters"]
+        check(n, u)
+
+
 def oracle_only(args):
     """The oracle's trajectory alone (any host), states saved for a later --load run."""
     from inputs import make
@@ -108,6 +120,7 @@ def main():
             json.dump(rec, f, indent=1)
 
     tlast = [time.perf_counter()]
+    cur_iters = []                           # oracle iteration counts of the step being checked
 
     def check(n, u):
         nonlocal ok
@@ -115,7 +128,7 @@ def main():
         rep = pb.step(args.scheme)
         got = [t.cpu().numpy() for t in pb.state()]
         row = {"step": n, "oracle_s": t_or, "gpu_ms": rep["ms"], "gpu_iters": list(rep["iters"]),
-               "oracle_iters": [op_iters[-1] for op_iters in iters_of()], "rel_l2": [], "oracle_norm": []}
+               "oracle_iters": list(cur_iters), "rel_l2": [], "oracle_norm": []}
         for a, ra in enumerate(lean.split(u)):
             nr = float(np.linalg.norm(ra))
             if nr == 0.0:
@@ -137,16 +150,17 @@ def main():
         # 537 MB matrix states do not fit and are recomputed here).  The oracle is bitwise
         # independent of the thread count (tests/test_oracle_fluxcg.py), so the mixed
         # trajectory is the oracle's own.
-        assert args.scheme == "D"
+        if args.scheme == "coupled":
+            load_coupled(args, lean, rec, check, tlast, cur_iters)
+            flush()
+            pb.close()
+            print("PASS" if ok else "FAIL", args.out)
+            sys.exit(0 if ok else 1)
         meta = json.load(open(os.path.join(args.load, f"config{args.config}_{args.scheme}.json")))
         pre = {r["step"]: r for r in meta["steps"]}
         st = fluxcg.DSchemeCG(lean, tau)
         rec["oracle"]["precomputed"] = dict(meta["oracle"], what=[])
         last_iters = [0] * lean.L
-
-        def iters_of():
-            return [[i] for i in last_iters]
-
         u = lean.u0.copy()
         tlast[0] = time.perf_counter()
         for n in range(1, args.steps + 1):
@@ -167,17 +181,15 @@ def main():
                     new[sl] = st.ops[a].solve(b[sl], u[sl], 1e-13)
                     last_iters[a] = st.ops[a].iters[-1]
             u = new
+            cur_iters[:] = last_iters
             check(n, u)
     else:
         st = fluxcg.DSchemeCG(lean, tau) if args.scheme == "D" else fluxcg.CoupledCG(lean, tau)
-
-        def iters_of():
-            return st.iters if args.scheme == "D" else [st.op.iters]
-
         u = lean.u0.copy()
         tlast[0] = time.perf_counter()
         for n in range(1, args.steps + 1):
             u = st.step(u)                       # the oracle's own trajectory
+            cur_iters[:] = [i[-1] for i in st.iters] if args.scheme == "D" else [st.op.iters[-1]]
             check(n, u)
     flush()
     pb.close()
