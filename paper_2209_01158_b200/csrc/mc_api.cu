@@ -108,6 +108,7 @@ struct mc_ctx {
   int32_t* perm[MC_MAX_CONTINUA] = {nullptr};   // graph: internal -> caller numbering
   double* bstat[MC_MAX_CONTINUA] = {nullptr};                // chunk-blocked streaming ELL pass: static blocks
   double* bstat16[MC_MAX_CONTINUA] = {nullptr};              //   compact static blocks (uint16 codes, D^-1 recomputed)
+  double* rrec[MC_MAX_CONTINUA][2] = {{nullptr, nullptr}};   // resident pass: published records (allocated on first use)
   double* bdyn[MC_MAX_CONTINUA][2] = {{nullptr, nullptr}};   //   and CG-state blocks (allocated on first use)
   double* tinv[MC_MAX_CONTINUA] = {nullptr};    // bj: chunk Thomas factors
   double* tcp[MC_MAX_CONTINUA] = {nullptr};
@@ -1340,8 +1341,20 @@ static mc_status enqueue_step(mc_ctx* c, int scheme, mc_step_report* rep_dev, cu
         P.cont[a].bjs = (!P.cont[a].bj && nconts == 1 && c->tinv[a] != nullptr && scheme != MC_COUPLED) ? 1 : 0;
         // streaming Jacobi pass of a decoupled solve: chunk-blocked workspace (the CG-state
         // blocks are allocated the first time a plan streams this network)
-        if (use_blocked() && c->bstat[a] && nconts == 1 && scheme != MC_COUPLED && P.cont[a].resident)
-          P.cont[a].bstat = c->bstat[a];          // resident pass on the blocked static data
+        if (use_blocked() && c->bstat[a] && nconts == 1 && scheme != MC_COUPLED && P.cont[a].resident) {
+          // resident pass on the blocked static data, publishing 32-byte records
+          if (!c->rrec[a][0]) {
+            const size_t cnt = (size_t)4 * ((size_t)c->hc[a].n + 64);
+            for (int k = 0; k < 2; ++k) {
+              mc_status st = dev_alloc(c, &c->rrec[a][k], cnt);
+              if (st != MC_OK) return st;
+              CUDA_TRY(c, cudaMemsetAsync(c->rrec[a][k], 0, cnt * 8, c->stream));
+            }
+          }
+          P.cont[a].bstat = c->bstat[a];
+          P.cont[a].rrec[0] = c->rrec[a][0];
+          P.cont[a].rrec[1] = c->rrec[a][1];
+        }
         if (use_blocked() && c->bstat[a] && nconts == 1 && scheme != MC_COUPLED && !P.cont[a].resident &&
             !P.cont[a].bj && !P.cont[a].bjs) {
           if (!c->bdyn[a][0]) {

@@ -94,6 +94,8 @@ struct ContDev {
   // chunk-blocked workspace of the streaming ELL pass of a decoupled Jacobi solve:
   const double* bstat;     // per 64-row chunk 256 doubles: D^-1 (64), shift (64), 4 int32 codes per row (128)
   const double* bstat16;   // compact static blocks, 128 doubles per chunk: shift (64), 4 uint16 codes per row (64)
+  double* rrec[2];         // resident pass: published 32-byte records {r, q, p, D^-1} per row (far gathers:
+                           // one 256-bit load of one sector instead of four 8-byte loads), by iteration parity
   double* bdyn[2];         // per chunk 192 doubles: r (64), q (64), p (64); double-buffered by iteration parity
   const double* tinv;      // bj: Thomas factors of each 64-row chunk's tridiagonal block:
   const double* tcp;       //     1 / pivot, super-diagonal multiplier c', sub-diagonal e_{i-1}

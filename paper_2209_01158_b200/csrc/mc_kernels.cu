@@ -62,6 +62,16 @@ __device__ __forceinline__ double pnew(double ro, double qo, double po, double d
   return __fma_rn(di, rn, __dmul_rn(b, po));
 }
 
+// 32-byte records {r, q, p, D^-1} published by the resident ELL pass: one 256-bit access each
+__device__ __forceinline__ void st_rec(double* rec, double r, double q, double p, double d) {
+  asm volatile("st.global.cg.v4.f64 [%0], {%1,%2,%3,%4};" ::"l"(rec), "d"(r), "d"(q), "d"(p), "d"(d) : "memory");
+}
+__device__ __forceinline__ double pn_rec(const double* rec, double a, double b) {
+  double r, q, p, d;
+  asm volatile("ld.global.cg.v4.f64 {%0,%1,%2,%3}, [%4];" : "=d"(r), "=d"(q), "=d"(p), "=d"(d) : "l"(rec) : "memory");
+  return pnew(r, q, p, d, a, b);
+}
+
 #if MC_PROF
 // dev instrumentation (-DMC_PROF=1 builds only): clock64 per phase of the CG loop,
 // summed over iterations by thread 0 of each group's first CTA
@@ -1068,13 +1078,15 @@ __device__ void iter_ells_res(const Ctx& c, const ContDev& C, int wg, int W, con
 // whole solve; far neighbours (slots 0 and 1 of a row; rarely 2 and 3) are gathered from
 // the previous iteration's r, q, p in global memory, in-chunk neighbours read the new p
 // from the slot.  r, p, q are published to global every iteration; x at the end.
-__device__ void iter_ells_res2(const Ctx& c, const ContDev& C, int wg, int W, const Stage& st, bool first,
+__device__ void iter_ells_res2(const Ctx& c, const ContDev& C, int wg, int W, const Stage& st, bool first, int s,
                                double (&acc)[kNPart]) {
   double* wsm = st.wsm;
   const int lane = threadIdx.x & 31;
   const int64_t off = C.off;
   const int r1 = (int)C.n;
   const int nch = (r1 + 63) / 64;
+  const double* recs = C.rrec[s];
+  double* recd = C.rrec[s ^ 1];
   if (first) {
     for (int m = wg, t = 0; m < nch; m += W, ++t) {
       double* sl = wsm + t * kSlotE;
@@ -1099,10 +1111,10 @@ __device__ void iter_ells_res2(const Ctx& c, const ContDev& C, int wg, int W, co
     const int4 c0 = *reinterpret_cast<const int4*>(sl + 128 + 4 * lane);
     const int4 c1 = *reinterpret_cast<const int4*>(sl + 128 + 4 * lane + 2);
     double f00 = 0.0, f01 = 0.0, f10 = 0.0, f11 = 0.0;
-    if (c0.x >= 0) f00 = c.pn_at(off + c0.x);
-    if (c0.y >= 0) f01 = c.pn_at(off + c0.y);
-    if (c1.x >= 0) f10 = c.pn_at(off + c1.x);
-    if (c1.y >= 0) f11 = c.pn_at(off + c1.y);
+    if (c0.x >= 0) f00 = pn_rec(recs + 4 * (int64_t)c0.x, c.a, c.b);
+    if (c0.y >= 0) f01 = pn_rec(recs + 4 * (int64_t)c0.y, c.a, c.b);
+    if (c1.x >= 0) f10 = pn_rec(recs + 4 * (int64_t)c1.x, c.a, c.b);
+    if (c1.y >= 0) f11 = pn_rec(recs + 4 * (int64_t)c1.y, c.a, c.b);
     const double2 di = *reinterpret_cast<const double2*>(sl + 2 * lane);
     const double2 ds = *reinterpret_cast<const double2*>(sl + 64 + 2 * lane);
     const double2 ro = *reinterpret_cast<const double2*>(sl + 256 + 2 * lane);
@@ -1116,22 +1128,15 @@ __device__ void iter_ells_res2(const Ctx& c, const ContDev& C, int wg, int W, co
     __syncwarp();                                                 // every lane has read the old p
     *reinterpret_cast<double2*>(sl + 384 + 2 * lane) = make_double2(p0, p1);
     const bool ok0 = base < r1, ok1 = base + 1 < r1;
-    if (ok1) {
-      st2mut(c.rd + g, make_double2(r0, r1n));
-      st2mut(c.pd + g, make_double2(p0, p1));
-    } else if (ok0) {
-      stmut(c.rd + g, r0);
-      stmut(c.pd + g, p0);
-    }
     __syncwarp();
     const double* pn = sl + 384;
     auto nbv = [&](int32_t cd, double far, double own) { return cd >= 0 ? far : (cd <= -2 ? pn[-2 - cd] : own); };
     double f02 = 0.0, f03 = 0.0, f12 = 0.0, f13 = 0.0;
     if (__any_sync(0xffffffffu, (c0.z >= 0) | (c0.w >= 0) | (c1.z >= 0) | (c1.w >= 0))) {   // rare: > 2 far in a row
-      if (c0.z >= 0) f02 = c.pn_at(off + c0.z);
-      if (c0.w >= 0) f03 = c.pn_at(off + c0.w);
-      if (c1.z >= 0) f12 = c.pn_at(off + c1.z);
-      if (c1.w >= 0) f13 = c.pn_at(off + c1.w);
+      if (c0.z >= 0) f02 = pn_rec(recs + 4 * (int64_t)c0.z, c.a, c.b);
+      if (c0.w >= 0) f03 = pn_rec(recs + 4 * (int64_t)c0.w, c.a, c.b);
+      if (c1.z >= 0) f12 = pn_rec(recs + 4 * (int64_t)c1.z, c.a, c.b);
+      if (c1.w >= 0) f13 = pn_rec(recs + 4 * (int64_t)c1.w, c.a, c.b);
     }
     double s0 = p0 - nbv(c0.x, f00, p0);
     s0 += p0 - nbv(c0.y, f01, p0);
@@ -1144,8 +1149,9 @@ __device__ void iter_ells_res2(const Ctx& c, const ContDev& C, int wg, int W, co
     const double q0 = __fma_rn(C.Tconst, s0, __dmul_rn(ds.x, p0));
     const double q1 = __fma_rn(C.Tconst, s1, __dmul_rn(ds.y, p1));
     *reinterpret_cast<double2*>(sl + 320 + 2 * lane) = make_double2(q0, q1);
-    if (ok1) st2mut(c.qd + g, make_double2(q0, q1));
-    else if (ok0) stmut(c.qd + g, q0);
+    // publish this iteration's records for the other warps' far gathers
+    if (ok0) st_rec(recd + 4 * (int64_t)base, r0, q0, p0, di.x);
+    if (ok1) st_rec(recd + 4 * (int64_t)(base + 1), r1n, q1, p1, di.y);
     if (ok0) c.accum(acc, p0, r0, di.x, q0);
     if (ok1) c.accum(acc, p1, r1n, di.y, q1);
   }
@@ -1296,7 +1302,7 @@ __device__ void iter_graph8(const Ctx& c, const ContDev& C, int r0, int r1,
 template <bool CPL>
 __device__ __forceinline__ void init_row(const StepParams& P, int64_t gi, double Ku_nb,
                                          const double* uo, double* x, int myphase, double (&acc)[3],
-                                         double* bw = nullptr) {
+                                         double* bw = nullptr, double* rw = nullptr) {
   const double u = uo[gi];
   double b = ldro(P.mtau + gi) * u + ldro(P.F + gi);
   double Ku = ldro((CPL ? P.dsC : P.dsD) + gi) * u + Ku_nb;
@@ -1322,6 +1328,7 @@ __device__ __forceinline__ void init_row(const StepParams& P, int64_t gi, double
   const double r = b - Ku;
   const double di = ldro(P.dinv + gi);
   x[gi] = u;
+  if (rw) st_rec(rw, r, 0.0, 0.0, di);       // resident pass: record for the first iteration's far gathers
   if (bw) {
     stmut(bw, r);
     stmut(bw + 64, 0.0);
@@ -1366,7 +1373,8 @@ __device__ void init_item(const StepParams& P, const Item& it, const double* uo,
         const double t = C.val ? ldro(C.val + e) : C.Tconst;
         s += t * (u - uo[ldro(C.col + e)]);
       }
-      init_row<CPL>(P, gi, s, uo, x, myphase, acc, (!CPL && C.bdyn[0]) ? C.bdyn[0] + (int64_t)(i >> 6) * kBDyn + (i & 63) : nullptr);
+      init_row<CPL>(P, gi, s, uo, x, myphase, acc, (!CPL && C.bdyn[0]) ? C.bdyn[0] + (int64_t)(i >> 6) * kBDyn + (i & 63) : nullptr,
+               (!CPL && C.rrec[0]) ? C.rrec[0] + 4 * (int64_t)i : nullptr);
     }
   }
 }
@@ -2097,7 +2105,7 @@ __device__ void run_group(const StepParams& P, int g, int cl, double* x, const d
       for (int k = 0; k < P.L; ++k)
         if (((G.cont_mask >> k) & 1) && P.cont[k].rr) {
           if (P.cont[k].resident) {
-            if (!CPL && P.cont[k].bstat) iter_ells_res2(c, P.cont[k], wg, W, st, j == 0, a5);
+            if (!CPL && P.cont[k].bstat) iter_ells_res2(c, P.cont[k], wg, W, st, j == 0, s, a5);
             else iter_ells_res<CPL>(c, P.cont[k], wg, W, st, j == 0, a5);
           } else if (!CPL && P.cont[k].bdyn[0]) {
             if (P.cont[k].bstat16) iter_ellb16(c, P.cont[k], wg, W, st, s, a5);
