@@ -242,7 +242,7 @@ def aggregate(world, dof, steps, total_ms):
 # oracle's own trajectory) for the configs whose full oracle step takes minutes to an hour:
 # measured by tests/tools/parity_full.py (profiles/r02_parity_config{2,4}_D.json).  Used only to
 # scale a bounded sample of oracle iterations to one whole step.
-ORACLE_ITERS = {2: [480, 430, 28000], 4: [400, 57000]}   # PLACEHOLDER until the parity records exist
+ORACLE_ITERS = {2: [362, 308, 29313], 4: [445, 74151]}
 
 
 def host_info():

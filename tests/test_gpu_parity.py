@@ -145,6 +145,44 @@ def test_config1_streaming_jacobi_ell_pass(torch_cuda):
     assert reps[1]["iters"][1] > 10000
 
 
+@pytest.mark.parametrize("env", [{}, {"MC_COMPACT": "0"}, {"MC_BLOCKED": "0"}])
+def test_streaming_pass_variants(torch_cuda, env):
+    """The three streaming passes of a decoupled Jacobi solve on a fracture network -- the
+    compact blocked pass (default: uint16 codes, D^-1 recomputed, 80 B per row), the blocked
+    pass with int32 codes (the fallback when a neighbour lies more than 127 chunks away) and
+    the pass on separate r, q, p arrays (fallback without blocked data, and the coupled
+    scheme's pass) -- each against the oracle at 1e-9: config 1's recipe on a 256^2 grid with
+    4 CTAs (132 chunks for 32 warps: every staging slot is refilled).  The pass is chosen at
+    load time, so each variant runs in a fresh process."""
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = (
+        "import sys, numpy as np\n"
+        f"sys.path.insert(0, {root!r})\n"
+        "from inputs import CONFIGS, make_fine\n"
+        "from oracle import assemble as asm, schemes\n"
+        "from paper_2209_01158_b200 import Problem\n"
+        "p = dict(CONFIGS[1]); p.pop('kind'); p.update(n=256, segments=100, lengths=(12, 100), NT=100)\n"
+        "scn = make_fine(**p)\n"
+        "sys_ = asm.assemble(scn)\n"
+        "ref = schemes.run(sys_, 'D', scn['T'] / scn['NT'], 5)\n"
+        "pb = Problem(scn, ctas=4)\n"
+        "worst = 0.0\n"
+        "for n in range(5):\n"
+        "    rep = pb.step('D')\n"
+        "    assert rep['paths'][1] == 1, rep['paths']\n"
+        "    got = [t.cpu().numpy() for t in pb.state()]\n"
+        "    for a, r in enumerate(sys_.split(ref[n])):\n"
+        "        nr = np.linalg.norm(r)\n"
+        "        worst = max(worst, np.linalg.norm(got[a] - r) / nr if nr > 0 else float(np.abs(got[a]).max()))\n"
+        "print('worst', worst, rep['iters'])\n"
+        "assert worst <= 1e-9, worst\n")
+    r = subprocess.run([sys.executable, "-c", code], env=dict(os.environ, **env), capture_output=True, text=True,
+                       timeout=900)
+    assert r.returncode == 0, r.stdout[-1500:] + r.stderr[-1500:]
+
+
 @pytest.mark.parametrize("scheme", ["D", "coupled"])
 def test_config2_standin_three_continua(torch_cuda, scheme):
     # config 2's recipe (3 continua, co-located + embedded transfer) on a 256^2 grid
