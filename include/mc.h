@@ -305,6 +305,11 @@ mc_status mc_nlmc_basis(const mc_nlmc* nl, int64_t r, double* psi);
 /* Device time (ms) of the basis kernel and of the projection kernel of the build. */
 mc_status mc_nlmc_times(const mc_nlmc* nl, double* ms_basis, double* ms_project);
 
+/* Cost model of the build: fp64 operations of the basis kernel (banded Cholesky,
+ * substitutions and Schur complement of Eq. eq:basis over all K_i^+) and
+ * the device bytes that hold the bases (per-region sparse storage + window maps). */
+mc_status mc_nlmc_cost(const mc_nlmc* nl, double* flops_basis, double* bytes_bases);
+
 const char* mc_nlmc_error_string(const mc_nlmc* nl);
 mc_status mc_nlmc_destroy(mc_nlmc* nl);
 

@@ -427,6 +427,8 @@ struct mc_nlmc {
   std::vector<int32_t> psi_dof0, psi_n;   // coarse DOF -> its region's slice of lglob
   std::vector<int32_t> lglob;        // region-local DOF -> global fine DOF
   double ms_basis = 0.0, ms_project = 0.0;
+  double flops_basis = 0.0;          // fp64 operations of the basis kernel (Cholesky, substitutions, Schur)
+  double bytes_bases = 0.0;          // device bytes that hold the bases and their window maps
 };
 
 namespace {
@@ -763,6 +765,14 @@ extern "C" mc_status mc_nlmc_build(mc_ctx* fine, const mc_nlmc_desc* d, mc_nlmc*
       delete nl;
       return ctx_error(fine, MC_ERR_ARG, msg);
     }
+    {
+      // fp64 operations of this region: banded Cholesky n (b+1)^2, forward + backward
+      // substitution of kc columns 4 n (b+1) kc, S = C Z 2 n kc, dense Cholesky kc^3 / 3,
+      // psi = Z S^-1 e per own DOF 2 kc^2 + 2 n kc
+      const double n_ = D.n, b_ = b + 1, k_ = D.kc;
+      nl->flops_basis += n_ * b_ * b_ + 4.0 * n_ * b_ * k_ + 2.0 * n_ * k_ + k_ * k_ * k_ / 3.0 +
+                         (double)D.nown * (2.0 * k_ * k_ + 2.0 * n_ * k_);
+    }
     dom.push_back(D);
   }
   // ---- device: bases
@@ -847,6 +857,7 @@ extern "C" mc_status mc_nlmc_build(mc_ctx* fine, const mc_nlmc_desc* d, mc_nlmc*
   // ---- the bases stay in their per-region storage (dpsi); project from it
   nl->psi_off = psi_off;
   nl->lglob = lglob;
+  nl->bytes_bases = 8.0 * (double)psi_len + 4.0 * (double)wmap.size();
   nl->psi_dof0.resize((size_t)nH);
   nl->psi_n.resize((size_t)nH);
   for (int64_t r = 0; r < nH; ++r) {
@@ -1010,6 +1021,13 @@ extern "C" mc_status mc_nlmc_basis(const mc_nlmc* nl, int64_t r, double* psi) {
   for (int32_t l = 0; l < n; ++l) out[(size_t)lg[l]] = loc[(size_t)l];
   return cudaMemcpy(psi, out.data(), (size_t)nl->N * sizeof(double), cudaMemcpyDefault) == cudaSuccess ? MC_OK
                                                                                                       : MC_ERR_CUDA;
+}
+
+extern "C" mc_status mc_nlmc_cost(const mc_nlmc* nl, double* flops_basis, double* bytes_bases) {
+  if (!nl) return MC_ERR_ARG;
+  if (flops_basis) *flops_basis = nl->flops_basis;
+  if (bytes_bases) *bytes_bases = nl->bytes_bases;
+  return MC_OK;
 }
 
 extern "C" mc_status mc_nlmc_times(const mc_nlmc* nl, double* ms_basis, double* ms_project) {

@@ -73,7 +73,7 @@ EXPORTS = ["mc_create", "mc_set_continuum", "mc_set_coupling", "mc_step_decouple
            "mc_step", "mc_set_permeability_order", "mc_set_preconditioner",
            "mc_run", "mc_get_state", "mc_set_state", "mc_size", "mc_last_kernel_ms", "mc_destroy",
            "mc_error_string", "mc_abi_version", "mc_nlmc_build", "mc_nlmc_sizes", "mc_nlmc_get",
-           "mc_nlmc_basis", "mc_nlmc_times", "mc_nlmc_error_string", "mc_nlmc_destroy"]
+           "mc_nlmc_basis", "mc_nlmc_times", "mc_nlmc_cost", "mc_nlmc_error_string", "mc_nlmc_destroy"]
 
 _lib = None
 
@@ -112,6 +112,7 @@ def load(path: str | None = None):
     lib.mc_nlmc_get.argtypes = [P] + [P] * 8
     lib.mc_nlmc_basis.argtypes = [P, _i64, P]
     lib.mc_nlmc_times.argtypes = [P, _pd, _pd]
+    lib.mc_nlmc_cost.argtypes = [P, _pd, _pd]
     lib.mc_nlmc_error_string.argtypes = [P]
     lib.mc_nlmc_error_string.restype = C.c_char_p
     lib.mc_nlmc_destroy.argtypes = [P]
@@ -402,6 +403,9 @@ class NlmcSpace:
         tb, tp = C.c_double(), C.c_double()
         self.lib.mc_nlmc_times(self.h, C.byref(tb), C.byref(tp))
         self.ms_basis, self.ms_project = tb.value, tp.value
+        fb, bb = C.c_double(), C.c_double()
+        self.lib.mc_nlmc_cost(self.h, C.byref(fb), C.byref(bb))
+        self.flops_basis, self.bytes_bases = fb.value, bb.value
         self.korder = pb.korder
 
     def basis(self, r):

@@ -41,6 +41,8 @@ for kind in ("2C", "3C"):
         wall = time.perf_counter() - t0
         row = dict(kind=kind, fine=scn["n"], coarse=nH, oversample=m, coarse_dofs=sp_.sizes,
                    nnz_per_row=sp_.nnz / sp_.n, ms_basis_kernel=sp_.ms_basis, ms_project_kernel=sp_.ms_project,
+                   basis_gflop=sp_.flops_basis / 1e9, basis_tflops=sp_.flops_basis / (sp_.ms_basis * 1e-3) / 1e12,
+                   bases_MB=sp_.bytes_bases / 1e6, dense_bases_MB_round1=8.0 * sp_.n * sp_.n_fine / 1e6,
                    s_build_wall=wall)
         cs = sp_.coarse_scenario(scn["T"], scn["NT"])
         pbar = np.bincount(sp_.fine_dof, weights=meas * fine_T, minlength=sp_.n) / \
