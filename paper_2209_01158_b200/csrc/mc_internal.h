@@ -59,9 +59,10 @@ constexpr int kPnBuf = 72;                 // ELL pass: new p of the chunk windo
 constexpr int kStagesB = MC_BJS_STAGES;    // streaming block-Jacobi passes: chunks in flight + 1
 constexpr int kStagesEB = (kStagesE > kStagesB) ? kStagesE : kStagesB;
 #ifndef MC_STAGES_C
-#define MC_STAGES_C 3
+#define MC_STAGES_C 2
 #endif
-constexpr int kStagesC = MC_STAGES_C;      // compact blocked pass (iter_ellb16): chunks in flight + 1
+constexpr int kStagesC = MC_STAGES_C;      // compact blocked pass (iter_ellb16): chunks in flight + 1 (3 measured
+                                           // slower than 2 on configs 2 and 4: the pass is DRAM-bound)
 constexpr int kSlotC = 384;                // its slot: 128 static + 192 CG state + 64 x
 constexpr int kMaxI(int a, int b) { return a > b ? a : b; }
 constexpr int kWarpSmem = kMaxI(kMaxI(kStages * kSlotG, kStagesEB * kSlotE), kStagesC * kSlotC) + kPnBuf;

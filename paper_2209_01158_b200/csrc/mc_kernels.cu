@@ -811,16 +811,45 @@ __device__ void iter_ellb(const Ctx& c, const ContDev& C, int wg, int W, const S
 // w = u & 63 (row in its chunk), (u >> 6) & 3 = the NEIGHBOUR's deg - 1, (u >> 8) - 127 =
 // its chunk relative to this one (0: this chunk, read the new p from the warp's buffer).
 // Built by finalize when every neighbour lies within 127 chunks (else bstat / iter_ellb).
+// Branch-free reciprocal (MUFU seed + two Newton steps, no special-case path: the diagonal
+// is a positive normal number, checked at setup).  Owners and far gatherers evaluate the same
+// instruction sequence on the same inputs, so they agree bitwise; the host's correctly
+// rounded 1/diag (init pass) may differ in the last bit, which only perturbs (r.z)_0.
 __device__ __forceinline__ double dinv_deg(double ds, int deg, double T) {
-  return __drcp_rn(__fma_rn(T, (double)deg, ds));
+  const double d = __fma_rn(T, (double)deg, ds);
+  double x;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(x) : "d"(d));
+  double e = __fma_rn(-d, x, 1.0);
+  x = __fma_rn(x, e, x);
+  e = __fma_rn(-d, x, 1.0);
+  return __fma_rn(x, e, x);
 }
-__device__ __forceinline__ double pn_blk16(const double* dyn, const double* stat, int m, unsigned u, double T,
-                                           double a, double b) {
+// Far gather in two phases, so that the loads of ALL far neighbours of a lane are in flight
+// before any arithmetic waits on them (with `if (far) value = f(loads)` per neighbour the
+// compiler emitted one branch region per neighbour: four serialised memory round trips).
+struct FarRaw {
+  double r, q, p, ds;
+};
+// predicated loads (no branch): r, q, p of row w of block `blk` (previous iteration), its shift
+__device__ __forceinline__ FarRaw far_load16(const double* dyn, const double* stat, int m, unsigned u, bool far) {
   const int64_t blk = (int64_t)m + (int)(u >> 8) - 127;
   const int w = u & 63;
   const double* d = dyn + blk * kBDyn + w;
-  const double di = dinv_deg(ldro(stat + blk * kBStat16 + w), (int)((u >> 6) & 3) + 1, T);
-  return pnew(ldnb(d), ldnb(d + 64), ldnb(d + 128), di, a, b);
+  const double* sp = stat + blk * kBStat16 + w;
+  FarRaw f;
+  f.r = f.q = f.p = 0.0;
+  f.ds = 1.0;
+  asm volatile(
+      "{\n .reg .pred pf;\n setp.ne.b32 pf, %6, 0;\n"
+      " @pf ld.global.f64 %0, [%4];\n @pf ld.global.f64 %1, [%4+512];\n @pf ld.global.f64 %2, [%4+1024];\n"
+      " @pf ld.global.nc.f64 %3, [%5];\n}"
+      : "+d"(f.r), "+d"(f.q), "+d"(f.p), "+d"(f.ds)
+      : "l"(d), "l"(sp), "r"((int)far)
+      : "memory");
+  return f;
+}
+__device__ __forceinline__ double far_pn16(const FarRaw& f, unsigned u, double T, double a, double b) {
+  return pnew(f.r, f.q, f.p, dinv_deg(f.ds, (int)((u >> 6) & 3) + 1, T), a, b);
 }
 
 __device__ void iter_ellb16(const Ctx& c, const ContDev& C, int wg, int W, const Stage& st, int s,
@@ -865,11 +894,10 @@ __device__ void iter_ellb16(const Ctx& c, const ContDev& C, int wg, int W, const
     const unsigned u00 = cw.x & 0xFFFFu, u01 = cw.x >> 16, u02 = cw.y & 0xFFFFu, u03 = cw.y >> 16;
     const unsigned u10 = cw.z & 0xFFFFu, u11 = cw.z >> 16, u12 = cw.w & 0xFFFFu, u13 = cw.w >> 16;
     // far neighbours (slots 0, 1 of each row): gathered in one batch, loads predicated per lane
-    double f00 = 0.0, f01 = 0.0, f10 = 0.0, f11 = 0.0;
-    if (isfar(u00)) f00 = pn_blk16(dyns, stat, m, u00, T, c.a, c.b);
-    if (isfar(u01)) f01 = pn_blk16(dyns, stat, m, u01, T, c.a, c.b);
-    if (isfar(u10)) f10 = pn_blk16(dyns, stat, m, u10, T, c.a, c.b);
-    if (isfar(u11)) f11 = pn_blk16(dyns, stat, m, u11, T, c.a, c.b);
+    const FarRaw g00 = far_load16(dyns, stat, m, u00, isfar(u00));
+    const FarRaw g01 = far_load16(dyns, stat, m, u01, isfar(u01));
+    const FarRaw g10 = far_load16(dyns, stat, m, u10, isfar(u10));
+    const FarRaw g11 = far_load16(dyns, stat, m, u11, isfar(u11));
     const double2 ds = *reinterpret_cast<const double2*>(sl + 2 * lane);
     const int deg0 = 4 - (int)none(u00) - (int)none(u01) - (int)none(u02) - (int)none(u03);
     const int deg1 = 4 - (int)none(u10) - (int)none(u11) - (int)none(u12) - (int)none(u13);
@@ -883,15 +911,19 @@ __device__ void iter_ellb16(const Ctx& c, const ContDev& C, int wg, int W, const
     __syncwarp();                                                 // previous chunk's pnb reads done
     *reinterpret_cast<double2*>(pnb + 2 * lane) = make_double2(p0, p1);
     __syncwarp();
+    const double f00 = far_pn16(g00, u00, T, c.a, c.b), f01 = far_pn16(g01, u01, T, c.a, c.b);
+    const double f10 = far_pn16(g10, u10, T, c.a, c.b), f11 = far_pn16(g11, u11, T, c.a, c.b);
     auto nbv = [&](unsigned u, double far, double own) {
       return none(u) ? own : ((u >> 8) == 127u ? pnb[u & 63u] : far);
     };
     double f02 = 0.0, f03 = 0.0, f12 = 0.0, f13 = 0.0;
     if (__any_sync(0xffffffffu, isfar(u02) | isfar(u03) | isfar(u12) | isfar(u13))) {   // rare: > 2 far in a row
-      if (isfar(u02)) f02 = pn_blk16(dyns, stat, m, u02, T, c.a, c.b);
-      if (isfar(u03)) f03 = pn_blk16(dyns, stat, m, u03, T, c.a, c.b);
-      if (isfar(u12)) f12 = pn_blk16(dyns, stat, m, u12, T, c.a, c.b);
-      if (isfar(u13)) f13 = pn_blk16(dyns, stat, m, u13, T, c.a, c.b);
+      const FarRaw g02 = far_load16(dyns, stat, m, u02, isfar(u02)), g03 = far_load16(dyns, stat, m, u03, isfar(u03));
+      const FarRaw g12 = far_load16(dyns, stat, m, u12, isfar(u12)), g13 = far_load16(dyns, stat, m, u13, isfar(u13));
+      f02 = far_pn16(g02, u02, T, c.a, c.b);
+      f03 = far_pn16(g03, u03, T, c.a, c.b);
+      f12 = far_pn16(g12, u12, T, c.a, c.b);
+      f13 = far_pn16(g13, u13, T, c.a, c.b);
     }
     double s0 = p0 - nbv(u00, f00, p0);
     s0 += p0 - nbv(u01, f01, p0);
