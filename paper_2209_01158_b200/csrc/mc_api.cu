@@ -1118,11 +1118,14 @@ static bool use_blocked() {
   return v;
 }
 
-// MC_COMPACT=0 (dev, A/B): 96-byte blocked pass (int32 codes, stored D^-1) instead of the 80-byte one
+// MC_COMPACT=1: the 80-byte compact blocked pass (uint16 codes, D^-1 recomputed) instead of the
+// 96-byte one.  Off by default: measured slower on config 4 (0.285 vs 0.261 ms per iteration,
+// profiles/r02_compact_pass.txt) -- the reciprocal lengthens the dependent chain behind the far
+// gathers, and with 16 warps per SM the 96-byte pass already runs at the DRAM ceiling.
 static bool use_compact() {
   static const bool v = [] {
     const char* e = getenv("MC_COMPACT");
-    return !(e && e[0] == '0');
+    return e && e[0] == '1';
   }();
   return v;
 }
