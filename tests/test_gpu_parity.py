@@ -183,6 +183,21 @@ def test_streaming_pass_variants(torch_cuda, env):
     assert r.returncode == 0, r.stdout[-1500:] + r.stderr[-1500:]
 
 
+@pytest.mark.parametrize("scheme", ["L", "U", "coupled"])
+def test_streaming_other_schemes(torch_cuda, scheme):
+    """The streamed network under the sequential L / U schemes (blocked pass, layer-n transfer
+    from the continua already solved) and the coupled scheme (pass on separate arrays with the
+    transfer in the operator), 4 CTAs, against the oracle."""
+    p = dict(CONFIGS[1])
+    p.pop("kind")
+    p.update(n=256, segments=100, lengths=(12, 100), NT=100)
+    scn = make_fine(**p)
+    got, reps = gpu_traj(scn, scheme, 4, ctas=4)
+    assert_parity(got, oracle_traj(scn, scheme, 4))
+    if scheme != "coupled":
+        assert reps[-1]["paths"][1] == 1
+
+
 @pytest.mark.parametrize("scheme", ["D", "coupled"])
 def test_config2_standin_three_continua(torch_cuda, scheme):
     # config 2's recipe (3 continua, co-located + embedded transfer) on a 256^2 grid
