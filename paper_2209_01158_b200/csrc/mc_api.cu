@@ -917,8 +917,8 @@ static mc_status finalize(mc_ctx* c) {
           }
         }
         UP(c->ecol[a], ell);
-        if (!H.bj) {
-          // chunk-blocked static data of the streaming pass (iter_ellb): per 64-row chunk
+        {
+          // chunk-blocked static data of the streaming passes (iter_ellb, bjs_pass_s2): per 64-row chunk
           // D^-1 (64) | D-scheme shift (64) | int32 codes [64][4], far neighbours first
           const int64_t nchk = (H.n + 63) / 64;
           std::vector<double> bst((size_t)nchk * kBStat, 0.0);
@@ -968,7 +968,7 @@ static mc_status finalize(mc_ctx* c) {
                 cp[k++] = (uint16_t)(((dch + 127) << 8) | ((degj - 1) << 6) | (j & 63));
               }
           }
-          if (fits && !H.anyfixed) UP(c->bstat16[a], b16);
+          if (fits && !H.anyfixed && !H.bj) UP(c->bstat16[a], b16);
         }
         if (H.bj) {
           // block-Jacobi: tridiagonal part of every 64-row chunk (rows i, i+1 of the
@@ -1383,6 +1383,7 @@ static mc_status enqueue_step(mc_ctx* c, int scheme, mc_step_report* rep_dev, cu
     c->path_mask |= path << (4 * a);
   }
   for (int a = 0; a < c->L; ++a) {
+    if (P.cont[a].bjs && use_blocked()) P.cont[a].bstat = c->bstat[a];   // pass S on the blocked codes
     P.cont[a].tinv = c->tinv[a];
     P.cont[a].tcp = c->tcp[a];
     P.cont[a].tem = c->tem[a];

@@ -1805,9 +1805,7 @@ __device__ void bjs_pass_u(const StepParams& P, const ContDev& C, int wg, int W,
   double* wsm = st.wsm;
   const int64_t off = C.off;
   const int r1 = (int)C.n, nch = (r1 + 63) / 64;
-  auto tix = [&](int m) { return (m / W) % kStagesB; };
-  auto prefetch = [&](int m) {
-    const int t = tix(m);
+  auto prefetch = [&](int m, int t) {
     double* sl = wsm + t * kSlotE;
     __syncwarp();
     if (lane == 0) {
@@ -1825,10 +1823,10 @@ __device__ void bjs_pass_u(const StepParams& P, const ContDev& C, int wg, int W,
   if (wg >= nch) return;
 #pragma unroll
   for (int k = 0; k < kStagesB - 1; ++k)
-    if (wg + k * W < nch) prefetch(wg + k * W);
-  for (int m = wg; m < nch; m += W) {
-    if (m + (kStagesB - 1) * W < nch) prefetch(m + (kStagesB - 1) * W);
-    const int t = tix(m);
+    if (wg + k * W < nch) prefetch(wg + k * W, k);
+  int t = 0;
+  for (int m = wg; m < nch; m += W, t = (t + 1 == kStagesB ? 0 : t + 1)) {
+    if (m + (kStagesB - 1) * W < nch) prefetch(m + (kStagesB - 1) * W, t == 0 ? kStagesB - 1 : t - 1);
     st.wait(t);
     double* sl = wsm + t * kSlotE;
     const int base = 64 * m + 2 * lane;
@@ -1978,6 +1976,86 @@ __device__ void bjs_pass_s(const StepParams& P, const ContDev& C, int wg, int W,
   }
 }
 
+// Pass S on the chunk-blocked static data (the shift and the far-first int32 codes of C.bstat;
+// no halo window: neighbours in other chunks are gathered, z and p_old from global).  Same
+// arithmetic as bjs_pass_s with three bulk copies per chunk instead of seven and without the
+// far-slot search cascades (the instruction diet of iter_ellb).
+__device__ void bjs_pass_s2(const StepParams& P, const ContDev& C, int wg, int W, const Stage& st,
+                            const double* zg, const double* pold, double* pnew_g, double beta, double (&a1)[1]) {
+  const int lane = threadIdx.x & 31;
+  double* wsm = st.wsm;
+  double* pnb = wsm + kWarpSmem - kPnBuf;
+  const int64_t off = C.off;
+  const int r1 = (int)C.n, nch = (r1 + 63) / 64;
+  const double* zo = zg + off;
+  const double* po_g = pold + off;
+  auto prefetch = [&](int m, int t) {
+    double* sl = wsm + t * kSlotE;
+    __syncwarp();
+    if (lane == 0) {
+      const int64_t g = off + 64 * (int64_t)m;
+      st.begin(t, 2u * 512u + 8u * 192u);
+      uint64_t* bar = st.bars + t;
+      bulk_g2s(sl, zg + g, 512, bar);
+      bulk_g2s(sl + 64, pold + g, 512, bar);
+      bulk_g2s(sl + 128, C.bstat + (int64_t)m * kBStat + 64, 8u * 192u, bar);   // shift (64) | codes (128)
+    }
+  };
+  if (wg >= nch) return;
+  prefetch(wg, 0);
+  int t = 0;
+  auto pfar = [&](int32_t j) { return __fma_rn(beta, ldnb(po_g + j), ldnb(zo + j)); };
+  for (int m = wg; m < nch; m += W, t ^= 1) {
+    if (m + W < nch) prefetch(m + W, t ^ 1);
+    st.wait(t);
+    const double* sl = wsm + t * kSlotE;
+    const int4 c0 = *reinterpret_cast<const int4*>(sl + 192 + 4 * lane);
+    const int4 c1 = *reinterpret_cast<const int4*>(sl + 192 + 4 * lane + 2);
+    double f00 = 0.0, f01 = 0.0, f10 = 0.0, f11 = 0.0;
+    if (c0.x >= 0) f00 = pfar(c0.x);
+    if (c0.y >= 0) f01 = pfar(c0.y);
+    if (c1.x >= 0) f10 = pfar(c1.x);
+    if (c1.y >= 0) f11 = pfar(c1.y);
+    const double2 z2 = *reinterpret_cast<const double2*>(sl + 2 * lane);
+    const double2 po = *reinterpret_cast<const double2*>(sl + 64 + 2 * lane);
+    const double2 ds = *reinterpret_cast<const double2*>(sl + 128 + 2 * lane);
+    const double p0 = __fma_rn(beta, po.x, z2.x), p1 = __fma_rn(beta, po.y, z2.y);
+    __syncwarp();                                                 // previous chunk's pnb reads done
+    *reinterpret_cast<double2*>(pnb + 2 * lane) = make_double2(p0, p1);
+    __syncwarp();
+    auto nbv = [&](int32_t cd, double far, double own) { return cd >= 0 ? far : (cd <= -2 ? pnb[-2 - cd] : own); };
+    double f02 = 0.0, f03 = 0.0, f12 = 0.0, f13 = 0.0;
+    if (__any_sync(0xffffffffu, (c0.z >= 0) | (c0.w >= 0) | (c1.z >= 0) | (c1.w >= 0))) {   // rare: > 2 far in a row
+      if (c0.z >= 0) f02 = pfar(c0.z);
+      if (c0.w >= 0) f03 = pfar(c0.w);
+      if (c1.z >= 0) f12 = pfar(c1.z);
+      if (c1.w >= 0) f13 = pfar(c1.w);
+    }
+    double s0 = p0 - nbv(c0.x, f00, p0);
+    s0 += p0 - nbv(c0.y, f01, p0);
+    s0 += p0 - nbv(c0.z, f02, p0);
+    s0 += p0 - nbv(c0.w, f03, p0);
+    double s1 = p1 - nbv(c1.x, f10, p1);
+    s1 += p1 - nbv(c1.y, f11, p1);
+    s1 += p1 - nbv(c1.z, f12, p1);
+    s1 += p1 - nbv(c1.w, f13, p1);
+    const double q0 = __fma_rn(C.Tconst, s0, __dmul_rn(ds.x, p0));
+    const double q1 = __fma_rn(C.Tconst, s1, __dmul_rn(ds.y, p1));
+    const int base = 64 * m + 2 * lane;
+    const int64_t g = off + base;
+    if (base + 1 < r1) {
+      st2mut(pnew_g + g, make_double2(p0, p1));
+      st2mut(P.q[0] + g, make_double2(q0, q1));
+      a1[0] += p0 * q0;
+      a1[0] += p1 * q1;
+    } else if (base < r1) {
+      stmut(pnew_g + g, p0);
+      stmut(P.q[0] + g, q0);
+      a1[0] += p0 * q0;
+    }
+  }
+}
+
 __device__ __noinline__ void run_group_bjs(const StepParams& P, int g, int cl, double* x, const double* uo) {
   const Group& G = P.grp[g];
   const int W = G.cta_count * kWarps;
@@ -2030,7 +2108,8 @@ __device__ __noinline__ void run_group_bjs(const StepParams& P, int g, int cl, d
       const double* pold = P.p[(j + 1) & 1];
       double a1[1] = {0.0};
       fence_proxy_async_shared_global();
-      bjs_pass_s(P, C, wg, W, st, zg, pold, pj, beta, a1);
+      if (C.bstat) bjs_pass_s2(P, C, wg, W, st, zg, pold, pj, beta, a1);
+      else bjs_pass_s(P, C, wg, W, st, zg, pold, pj, beta, a1);
       double t1[1];
       group_allreduce<1>(P, g, cl, epoch, a1, t1);
       if (!(t1[0] > 0.0)) {
