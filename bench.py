@@ -471,7 +471,7 @@ def main():
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline_leg(args, scn, reps)
     if rank == 0:
-        l2res = all(p["path"] in ("ell-resident", "bj-resident") or p["rows"] * 96 < 100e6 for p in per_solve) \
+        l2res = all(p["path"] in ("ell-resident", "bj-resident") or p["rows"] * 96 < 120e6 for p in per_solve) \
             if per_solve else False
         line = {
             "metric": "fine-grid DOF-steps/s (decoupled, fp64)" if args.scheme == "D" else
