@@ -36,8 +36,10 @@ using namespace mc;
 namespace {
 
 constexpr int64_t kLargeRows = int64_t(2) << 20;   // "bandwidth-bound" solve
+#if MC_CHECK
 constexpr size_t kGuardBytes = 256;
 constexpr int kGuardByte = 0xA5;
+#endif
 constexpr int kPlanSteps = 3;                        // D-scheme steps after which the CTA plan is frozen
 constexpr int kRunBatch = 256;                       // mc_run: steps enqueued per synchronisation
 constexpr int64_t kOneCtaWork = 0;                   // rows + stored entries below which a solve gets one CTA
@@ -865,13 +867,7 @@ static mc_status finalize(mc_ctx* c) {
     for (int64_t i = 0; i < c->hc[a].n; ++i) {
       const size_t g = (size_t)(c->off[a] + i);
       dsD[g] = dbase[g] + sig[g];
-      // diag(K), Jacobi (reading C14).  A network with one transmissibility T and <= 4
-      // neighbours per row: ds + T deg in one rounding -- the streaming pass recomputes
-      // exactly this from ds and the neighbour count (iter_ellb16)
-      const HostCont& Hc = c->hc[a];
-      const bool ellu = Hc.kind == KIND_GRAPH && Hc.val.empty() && Hc.maxdeg <= 4 && !Hc.bj && !Hc.anyfixed;
-      const double diag = ellu ? std::fma(Hc.Tconst, (double)(Hc.rowptr[(size_t)i + 1] - Hc.rowptr[(size_t)i]), dsD[g])
-                               : dsD[g] + tsum[g];
+      const double diag = dsD[g] + tsum[g];            // diag(K), Jacobi (reading C14)
       if (!(diag > 0.0) || !std::isfinite(diag))
         return fail(c, MC_ERR_ARG, "continuum %d row %lld: diagonal %g of M/tau + A is not > 0", a,
                     (long long)i, diag);
@@ -941,18 +937,19 @@ static mc_status finalize(mc_ctx* c) {
               }
           }
           UP(c->bstat[a], bst);
-          // compact blocks (iter_ellb16): shift (64) | uint16 codes [64][4]; only when every
-          // neighbour lies within 127 chunks of its row
+          // compact blocks (iter_ellb16): D^-1 (64) | shift (64) | uint16 codes [64][4]; only when
+          // every neighbour lies within 127 chunks of its row
           std::vector<double> b16((size_t)nchk * kBStat16, 0.0);
           bool fits = true;
           for (int64_t m = 0; m < nchk; ++m) {
-            uint16_t* cp = reinterpret_cast<uint16_t*>(&b16[(size_t)(m * kBStat16 + 64)]);
+            uint16_t* cp = reinterpret_cast<uint16_t*>(&b16[(size_t)(m * kBStat16 + 128)]);
             for (int q = 0; q < 256; ++q) cp[q] = 0xFFFFu;
           }
           for (int64_t i = 0; i < H.n && fits; ++i) {
             const int64_t m = i >> 6, w = i & 63;
-            b16[(size_t)(m * kBStat16 + w)] = dsD[(size_t)(c->off[a] + i)];
-            uint16_t* cp = reinterpret_cast<uint16_t*>(&b16[(size_t)(m * kBStat16 + 64)]) + 4 * w;
+            b16[(size_t)(m * kBStat16 + w)] = dinv[(size_t)(c->off[a] + i)];
+            b16[(size_t)(m * kBStat16 + 64 + w)] = dsD[(size_t)(c->off[a] + i)];
+            uint16_t* cp = reinterpret_cast<uint16_t*>(&b16[(size_t)(m * kBStat16 + 128)]) + 4 * w;
             int k = 0;
             for (int pass = 0; pass < 2; ++pass)                 // far neighbours first
               for (int32_t e = H.rowptr[(size_t)i]; e < H.rowptr[(size_t)i + 1]; ++e) {
@@ -1118,14 +1115,11 @@ static bool use_blocked() {
   return v;
 }
 
-// MC_COMPACT=1: the 80-byte compact blocked pass (uint16 codes, D^-1 recomputed) instead of the
-// 96-byte one.  Off by default: measured slower on config 4 (0.285 vs 0.261 ms per iteration,
-// profiles/r02_compact_pass.txt) -- the reciprocal lengthens the dependent chain behind the far
-// gathers, and with 16 warps per SM the 96-byte pass already runs at the DRAM ceiling.
+// MC_COMPACT=0 (dev, A/B): the 96-byte blocked pass (int32 codes) instead of the 88-byte compact one
 static bool use_compact() {
   static const bool v = [] {
     const char* e = getenv("MC_COMPACT");
-    return e && e[0] == '1';
+    return !(e && e[0] == '0');
   }();
   return v;
 }

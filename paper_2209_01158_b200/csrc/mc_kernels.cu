@@ -803,54 +803,37 @@ __device__ void iter_ellb(const Ctx& c, const ContDev& C, int wg, int W, const S
   }
 }
 
-// Compact variant of iter_ellb (80 instead of 96 B per row and iteration): the static block
-// is 128 doubles -- the D-scheme shift ds (64) and four uint16 codes per row (64) -- and
-// D^-1 = 1 / (ds + T deg) is recomputed (the network has one transmissibility T, deg = the
-// row's neighbour count; finalize stores exactly this value in P.dinv, so owners, far
-// gatherers and the init pass all use the same bits).  Code u: 0xFFFF none; otherwise
-// w = u & 63 (row in its chunk), (u >> 6) & 3 = the NEIGHBOUR's deg - 1, (u >> 8) - 127 =
-// its chunk relative to this one (0: this chunk, read the new p from the warp's buffer).
-// Built by finalize when every neighbour lies within 127 chunks (else bstat / iter_ellb).
-// Branch-free reciprocal (MUFU seed + two Newton steps, no special-case path: the diagonal
-// is a positive normal number, checked at setup).  Owners and far gatherers evaluate the same
-// instruction sequence on the same inputs, so they agree bitwise; the host's correctly
-// rounded 1/diag (init pass) may differ in the last bit, which only perturbs (r.z)_0.
-__device__ __forceinline__ double dinv_deg(double ds, int deg, double T) {
-  const double d = __fma_rn(T, (double)deg, ds);
-  double x;
-  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(x) : "d"(d));
-  double e = __fma_rn(-d, x, 1.0);
-  x = __fma_rn(x, e, x);
-  e = __fma_rn(-d, x, 1.0);
-  return __fma_rn(x, e, x);
-}
+// Compact variant of iter_ellb (88 instead of 96 B per row and iteration): the codes of the
+// static block are uint16 -- 0xFFFF none; otherwise w = u & 63 (row in its chunk) and
+// (u >> 8) - 127 = the neighbour's chunk relative to this one (0: this chunk, read the new p
+// from the warp's buffer); bits 6-7 carry the neighbour's degree - 1 (unused here).  Block:
+// D^-1 (64) | shift (64) | codes [64][4] (64 doubles).  Built by finalize when every neighbour
+// lies within 127 chunks (else bstat / iter_ellb).  (A version that also dropped D^-1 and
+// recomputed it as 1 / (shift + T deg), 80 B per row, measured slower: the reciprocal sits
+// behind the far gathers -- profiles/r02_compact_pass.txt.)
 // Far gather in two phases, so that the loads of ALL far neighbours of a lane are in flight
-// before any arithmetic waits on them (with `if (far) value = f(loads)` per neighbour the
-// compiler emitted one branch region per neighbour: four serialised memory round trips).
+// before any arithmetic waits on them.
 struct FarRaw {
-  double r, q, p, ds;
+  double r, q, p, d;
 };
-// predicated loads (no branch): r, q, p of row w of block `blk` (previous iteration), its shift
+// predicated loads (no branch): r, q, p of row w of block `blk` (previous iteration), its D^-1
 __device__ __forceinline__ FarRaw far_load16(const double* dyn, const double* stat, int m, unsigned u, bool far) {
   const int64_t blk = (int64_t)m + (int)(u >> 8) - 127;
   const int w = u & 63;
   const double* d = dyn + blk * kBDyn + w;
   const double* sp = stat + blk * kBStat16 + w;
   FarRaw f;
-  f.r = f.q = f.p = 0.0;
-  f.ds = 1.0;
+  f.r = f.q = f.p = f.d = 0.0;
   asm volatile(
       "{\n .reg .pred pf;\n setp.ne.b32 pf, %6, 0;\n"
       " @pf ld.global.f64 %0, [%4];\n @pf ld.global.f64 %1, [%4+512];\n @pf ld.global.f64 %2, [%4+1024];\n"
       " @pf ld.global.nc.f64 %3, [%5];\n}"
-      : "+d"(f.r), "+d"(f.q), "+d"(f.p), "+d"(f.ds)
+      : "+d"(f.r), "+d"(f.q), "+d"(f.p), "+d"(f.d)
       : "l"(d), "l"(sp), "r"((int)far)
       : "memory");
   return f;
 }
-__device__ __forceinline__ double far_pn16(const FarRaw& f, unsigned u, double T, double a, double b) {
-  return pnew(f.r, f.q, f.p, dinv_deg(f.ds, (int)((u >> 6) & 3) + 1, T), a, b);
-}
+__device__ __forceinline__ double far_pn16(const FarRaw& f, double a, double b) { return pnew(f.r, f.q, f.p, f.d, a, b); }
 
 __device__ void iter_ellb16(const Ctx& c, const ContDev& C, int wg, int W, const Stage& st, int s,
                             double (&acc)[kNPart]) {
@@ -890,7 +873,7 @@ __device__ void iter_ellb16(const Ctx& c, const ContDev& C, int wg, int W, const
     st.wait(t);
     const double* sl = wsm + t * kSlotC;
     // codes of rows 2 lane, 2 lane + 1: 8 consecutive uint16
-    const uint4 cw = *reinterpret_cast<const uint4*>(sl + 64 + 2 * lane);
+    const uint4 cw = *reinterpret_cast<const uint4*>(sl + 128 + 2 * lane);
     const unsigned u00 = cw.x & 0xFFFFu, u01 = cw.x >> 16, u02 = cw.y & 0xFFFFu, u03 = cw.y >> 16;
     const unsigned u10 = cw.z & 0xFFFFu, u11 = cw.z >> 16, u12 = cw.w & 0xFFFFu, u13 = cw.w >> 16;
     // far neighbours (slots 0, 1 of each row): gathered in one batch, loads predicated per lane
@@ -898,10 +881,9 @@ __device__ void iter_ellb16(const Ctx& c, const ContDev& C, int wg, int W, const
     const FarRaw g01 = far_load16(dyns, stat, m, u01, isfar(u01));
     const FarRaw g10 = far_load16(dyns, stat, m, u10, isfar(u10));
     const FarRaw g11 = far_load16(dyns, stat, m, u11, isfar(u11));
-    const double2 ds = *reinterpret_cast<const double2*>(sl + 2 * lane);
-    const int deg0 = 4 - (int)none(u00) - (int)none(u01) - (int)none(u02) - (int)none(u03);
-    const int deg1 = 4 - (int)none(u10) - (int)none(u11) - (int)none(u12) - (int)none(u13);
-    const double di0 = dinv_deg(ds.x, deg0, T), di1 = dinv_deg(ds.y, deg1, T);
+    const double2 di = *reinterpret_cast<const double2*>(sl + 2 * lane);
+    const double2 ds = *reinterpret_cast<const double2*>(sl + 64 + 2 * lane);
+    const double di0 = di.x, di1 = di.y;
     const double2 ro = *reinterpret_cast<const double2*>(sl + kBStat16 + 2 * lane);
     const double2 qo = *reinterpret_cast<const double2*>(sl + kBStat16 + 64 + 2 * lane);
     const double2 po = *reinterpret_cast<const double2*>(sl + kBStat16 + 128 + 2 * lane);
@@ -911,8 +893,8 @@ __device__ void iter_ellb16(const Ctx& c, const ContDev& C, int wg, int W, const
     __syncwarp();                                                 // previous chunk's pnb reads done
     *reinterpret_cast<double2*>(pnb + 2 * lane) = make_double2(p0, p1);
     __syncwarp();
-    const double f00 = far_pn16(g00, u00, T, c.a, c.b), f01 = far_pn16(g01, u01, T, c.a, c.b);
-    const double f10 = far_pn16(g10, u10, T, c.a, c.b), f11 = far_pn16(g11, u11, T, c.a, c.b);
+    const double f00 = far_pn16(g00, c.a, c.b), f01 = far_pn16(g01, c.a, c.b);
+    const double f10 = far_pn16(g10, c.a, c.b), f11 = far_pn16(g11, c.a, c.b);
     auto nbv = [&](unsigned u, double far, double own) {
       return none(u) ? own : ((u >> 8) == 127u ? pnb[u & 63u] : far);
     };
@@ -920,10 +902,10 @@ __device__ void iter_ellb16(const Ctx& c, const ContDev& C, int wg, int W, const
     if (__any_sync(0xffffffffu, isfar(u02) | isfar(u03) | isfar(u12) | isfar(u13))) {   // rare: > 2 far in a row
       const FarRaw g02 = far_load16(dyns, stat, m, u02, isfar(u02)), g03 = far_load16(dyns, stat, m, u03, isfar(u03));
       const FarRaw g12 = far_load16(dyns, stat, m, u12, isfar(u12)), g13 = far_load16(dyns, stat, m, u13, isfar(u13));
-      f02 = far_pn16(g02, u02, T, c.a, c.b);
-      f03 = far_pn16(g03, u03, T, c.a, c.b);
-      f12 = far_pn16(g12, u12, T, c.a, c.b);
-      f13 = far_pn16(g13, u13, T, c.a, c.b);
+      f02 = far_pn16(g02, c.a, c.b);
+      f03 = far_pn16(g03, c.a, c.b);
+      f12 = far_pn16(g12, c.a, c.b);
+      f13 = far_pn16(g13, c.a, c.b);
     }
     double s0 = p0 - nbv(u00, f00, p0);
     s0 += p0 - nbv(u01, f01, p0);
@@ -1139,7 +1121,6 @@ __device__ void iter_ells_res2(const Ctx& c, const ContDev& C, int wg, int W, co
   for (int m = wg, t = 0; m < nch; m += W, ++t) {
     double* sl = wsm + t * kSlotE;
     const int base = 64 * m + 2 * lane;
-    const int64_t g = off + base;
     const int4 c0 = *reinterpret_cast<const int4*>(sl + 128 + 4 * lane);
     const int4 c1 = *reinterpret_cast<const int4*>(sl + 128 + 4 * lane + 2);
     double f00 = 0.0, f01 = 0.0, f10 = 0.0, f11 = 0.0;
