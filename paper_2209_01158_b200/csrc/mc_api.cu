@@ -109,7 +109,6 @@ struct mc_ctx {
   int32_t* ecol[MC_MAX_CONTINUA] = {nullptr};
   int32_t* perm[MC_MAX_CONTINUA] = {nullptr};   // graph: internal -> caller numbering
   double* bstat[MC_MAX_CONTINUA] = {nullptr};                // chunk-blocked streaming ELL pass: static blocks
-  double* bstat16[MC_MAX_CONTINUA] = {nullptr};              //   compact static blocks (uint16 codes, D^-1 recomputed)
   double* rrec[MC_MAX_CONTINUA][2] = {{nullptr, nullptr}};   // resident pass: published records (allocated on first use)
   double* bdyn[MC_MAX_CONTINUA][2] = {{nullptr, nullptr}};   //   and CG-state blocks (allocated on first use)
   double* tinv[MC_MAX_CONTINUA] = {nullptr};    // bj: chunk Thomas factors
@@ -937,35 +936,6 @@ static mc_status finalize(mc_ctx* c) {
               }
           }
           UP(c->bstat[a], bst);
-          // compact blocks (iter_ellb16): D^-1 (64) | shift (64) | uint16 codes [64][4]; only when
-          // every neighbour lies within 127 chunks of its row
-          std::vector<double> b16((size_t)nchk * kBStat16, 0.0);
-          bool fits = true;
-          for (int64_t m = 0; m < nchk; ++m) {
-            uint16_t* cp = reinterpret_cast<uint16_t*>(&b16[(size_t)(m * kBStat16 + 128)]);
-            for (int q = 0; q < 256; ++q) cp[q] = 0xFFFFu;
-          }
-          for (int64_t i = 0; i < H.n && fits; ++i) {
-            const int64_t m = i >> 6, w = i & 63;
-            b16[(size_t)(m * kBStat16 + w)] = dinv[(size_t)(c->off[a] + i)];
-            b16[(size_t)(m * kBStat16 + 64 + w)] = dsD[(size_t)(c->off[a] + i)];
-            uint16_t* cp = reinterpret_cast<uint16_t*>(&b16[(size_t)(m * kBStat16 + 128)]) + 4 * w;
-            int k = 0;
-            for (int pass = 0; pass < 2; ++pass)                 // far neighbours first
-              for (int32_t e = H.rowptr[(size_t)i]; e < H.rowptr[(size_t)i + 1]; ++e) {
-                const int64_t j = H.col[(size_t)e];
-                const int64_t dch = (j >> 6) - m;
-                const bool far = dch != 0;
-                if (far != (pass == 0)) continue;
-                if (dch < -127 || dch > 127) {
-                  fits = false;
-                  break;
-                }
-                const int degj = H.rowptr[(size_t)j + 1] - H.rowptr[(size_t)j];
-                cp[k++] = (uint16_t)(((dch + 127) << 8) | ((degj - 1) << 6) | (j & 63));
-              }
-          }
-          if (fits && !H.anyfixed && !H.bj) UP(c->bstat16[a], b16);
         }
         if (H.bj) {
           // block-Jacobi: tridiagonal part of every 64-row chunk (rows i, i+1 of the
@@ -1110,15 +1080,6 @@ static int64_t one_cta_work() {
 static bool use_blocked() {
   static const bool v = [] {
     const char* e = getenv("MC_BLOCKED");
-    return !(e && e[0] == '0');
-  }();
-  return v;
-}
-
-// MC_COMPACT=0 (dev, A/B): the 96-byte blocked pass (int32 codes) instead of the 88-byte compact one
-static bool use_compact() {
-  static const bool v = [] {
-    const char* e = getenv("MC_COMPACT");
     return !(e && e[0] == '0');
   }();
   return v;
@@ -1363,7 +1324,6 @@ static mc_status enqueue_step(mc_ctx* c, int scheme, mc_step_report* rep_dev, cu
             }
           }
           P.cont[a].bstat = c->bstat[a];
-          P.cont[a].bstat16 = use_compact() ? c->bstat16[a] : nullptr;
           P.cont[a].bdyn[0] = c->bdyn[a][0];
           P.cont[a].bdyn[1] = c->bdyn[a][1];
         }

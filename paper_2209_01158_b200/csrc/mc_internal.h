@@ -50,7 +50,6 @@ constexpr int kSlotG = 536;            // grid strip slot: 8 arrays x 64 doubles
 constexpr int kSlotE = 528;            // ELL chunk slot: r, q, p, D^-1 windows (68), x, shift (64), 4 x 64 int32 codes
 constexpr int kStagesE = 2;                // ELL pass: chunk in flight + chunk computed
 constexpr int kBStat = 256;                // chunk-blocked pass: doubles of static data per chunk
-constexpr int kBStat16 = 192;              //   compact variant: D^-1 (64) | shift (64) | uint16 codes [64][4] (64)
 constexpr int kBDyn = 192;                 //                     doubles of CG state per chunk and parity
 constexpr int kPnBuf = 72;                 // ELL pass: new p of the chunk window (68) per warp
 #ifndef MC_BJS_STAGES
@@ -58,16 +57,10 @@ constexpr int kPnBuf = 72;                 // ELL pass: new p of the chunk windo
 #endif
 constexpr int kStagesB = MC_BJS_STAGES;    // streaming block-Jacobi passes: chunks in flight + 1
 constexpr int kStagesEB = (kStagesE > kStagesB) ? kStagesE : kStagesB;
-#ifndef MC_STAGES_C
-#define MC_STAGES_C 2
-#endif
-constexpr int kStagesC = MC_STAGES_C;      // compact blocked pass (iter_ellb16): chunks in flight + 1 (3 measured
-                                           // slower than 2 on configs 2 and 4: the pass is DRAM-bound)
-constexpr int kSlotC = 448;                // its slot: 192 static + 192 CG state + 64 x
 constexpr int kMaxI(int a, int b) { return a > b ? a : b; }
-constexpr int kWarpSmem = kMaxI(kMaxI(kStages * kSlotG, kStagesEB * kSlotE), kStagesC * kSlotC) + kPnBuf;
+constexpr int kWarpSmem = kMaxI(kStages * kSlotG, kStagesEB * kSlotE) + kPnBuf;
 // bytes per CTA: staging slots, then one mbarrier per slot per warp, then a parity word per warp
-constexpr int kNBars = kMaxI(kMaxI(kStages, kStagesEB), kStagesC);   // mbarriers per warp
+constexpr int kNBars = kMaxI(kStages, kStagesEB);   // mbarriers per warp
 constexpr int kDynSmem = kWarps * kWarpSmem * 8 + kWarps * kNBars * 8 + kWarps * 8;
 
 enum ContKind : int32_t { KIND_GRID = 0, KIND_GRAPH = 1 };
@@ -94,7 +87,6 @@ struct ContDev {
   int32_t bjs;             // block-Jacobi, streaming passes (network too large to stay resident)
   // chunk-blocked workspace of the streaming ELL pass of a decoupled Jacobi solve:
   const double* bstat;     // per 64-row chunk 256 doubles: D^-1 (64), shift (64), 4 int32 codes per row (128)
-  const double* bstat16;   // compact static blocks, 192 doubles per chunk: D^-1 (64), shift (64), 4 uint16 codes per row (64)
   double* rrec[2];         // resident pass: published 32-byte records {r, q, p, D^-1} per row (far gathers:
                            // one 256-bit load of one sector instead of four 8-byte loads), by iteration parity
   double* bdyn[2];         // per chunk 192 doubles: r (64), q (64), p (64); double-buffered by iteration parity

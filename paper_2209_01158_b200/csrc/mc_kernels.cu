@@ -803,137 +803,6 @@ __device__ void iter_ellb(const Ctx& c, const ContDev& C, int wg, int W, const S
   }
 }
 
-// Compact variant of iter_ellb (88 instead of 96 B per row and iteration): the codes of the
-// static block are uint16 -- 0xFFFF none; otherwise w = u & 63 (row in its chunk) and
-// (u >> 8) - 127 = the neighbour's chunk relative to this one (0: this chunk, read the new p
-// from the warp's buffer); bits 6-7 carry the neighbour's degree - 1 (unused here).  Block:
-// D^-1 (64) | shift (64) | codes [64][4] (64 doubles).  Built by finalize when every neighbour
-// lies within 127 chunks (else bstat / iter_ellb).  (A version that also dropped D^-1 and
-// recomputed it as 1 / (shift + T deg), 80 B per row, measured slower: the reciprocal sits
-// behind the far gathers -- profiles/r02_compact_pass.txt.)
-// Far gather in two phases, so that the loads of ALL far neighbours of a lane are in flight
-// before any arithmetic waits on them.
-struct FarRaw {
-  double r, q, p, d;
-};
-// predicated loads (no branch): r, q, p of row w of block `blk` (previous iteration), its D^-1
-__device__ __forceinline__ FarRaw far_load16(const double* dyn, const double* stat, int m, unsigned u, bool far) {
-  const int64_t blk = (int64_t)m + (int)(u >> 8) - 127;
-  const int w = u & 63;
-  const double* d = dyn + blk * kBDyn + w;
-  const double* sp = stat + blk * kBStat16 + w;
-  FarRaw f;
-  f.r = f.q = f.p = f.d = 0.0;
-  asm volatile(
-      "{\n .reg .pred pf;\n setp.ne.b32 pf, %6, 0;\n"
-      " @pf ld.global.f64 %0, [%4];\n @pf ld.global.f64 %1, [%4+512];\n @pf ld.global.f64 %2, [%4+1024];\n"
-      " @pf ld.global.nc.f64 %3, [%5];\n}"
-      : "+d"(f.r), "+d"(f.q), "+d"(f.p), "+d"(f.d)
-      : "l"(d), "l"(sp), "r"((int)far)
-      : "memory");
-  return f;
-}
-__device__ __forceinline__ double far_pn16(const FarRaw& f, double a, double b) { return pnew(f.r, f.q, f.p, f.d, a, b); }
-
-__device__ void iter_ellb16(const Ctx& c, const ContDev& C, int wg, int W, const Stage& st, int s,
-                            double (&acc)[kNPart]) {
-  double* wsm = st.wsm;
-  double* pnb = wsm + kWarpSmem - kPnBuf;                      // new p of the chunk's rows
-  const int lane = threadIdx.x & 31;
-  const int r1 = (int)C.n;
-  const int nch = (r1 + 63) / 64;
-  const double* stat = C.bstat16;
-  const double* dyns = C.bdyn[s];
-  double* dynd = C.bdyn[s ^ 1];
-  double* xg = c.x + C.off;
-  const double T = C.Tconst;
-  auto prefetch = [&](int m, int t) {
-    double* sl = wsm + t * kSlotC;
-    __syncwarp();
-    if (lane == 0) {
-      st.begin(t, 8u * (kBStat16 + kBDyn + 64));
-      uint64_t* bar = st.bars + t;
-      bulk_g2s(sl, stat + (int64_t)m * kBStat16, 8u * kBStat16, bar);
-      bulk_g2s(sl + kBStat16, dyns + (int64_t)m * kBDyn, 8u * kBDyn, bar);
-      bulk_g2s(sl + kBStat16 + kBDyn, xg + 64 * (int64_t)m, 512, bar);
-    }
-  };
-  if (wg >= nch) return;
-#pragma unroll
-  for (int d = 0; d < kStagesC - 1; ++d)
-    if (wg + d * W < nch) prefetch(wg + d * W, d);                // kStagesC - 1 chunks in flight
-  int t = 0;
-  auto none = [](unsigned u) { return u == 0xFFFFu; };
-  auto isfar = [](unsigned u) { return u != 0xFFFFu && (u >> 8) != 127u; };
-  for (int m = wg; m < nch; m += W, t = (t + 1 == kStagesC ? 0 : t + 1)) {
-    {
-      const int tn = t + kStagesC - 1 >= kStagesC ? t - 1 : t + kStagesC - 1;   // slot freed by the previous chunk
-      if (m + (kStagesC - 1) * W < nch) prefetch(m + (kStagesC - 1) * W, tn);
-    }
-    st.wait(t);
-    const double* sl = wsm + t * kSlotC;
-    // codes of rows 2 lane, 2 lane + 1: 8 consecutive uint16
-    const uint4 cw = *reinterpret_cast<const uint4*>(sl + 128 + 2 * lane);
-    const unsigned u00 = cw.x & 0xFFFFu, u01 = cw.x >> 16, u02 = cw.y & 0xFFFFu, u03 = cw.y >> 16;
-    const unsigned u10 = cw.z & 0xFFFFu, u11 = cw.z >> 16, u12 = cw.w & 0xFFFFu, u13 = cw.w >> 16;
-    // far neighbours (slots 0, 1 of each row): gathered in one batch, loads predicated per lane
-    const FarRaw g00 = far_load16(dyns, stat, m, u00, isfar(u00));
-    const FarRaw g01 = far_load16(dyns, stat, m, u01, isfar(u01));
-    const FarRaw g10 = far_load16(dyns, stat, m, u10, isfar(u10));
-    const FarRaw g11 = far_load16(dyns, stat, m, u11, isfar(u11));
-    const double2 di = *reinterpret_cast<const double2*>(sl + 2 * lane);
-    const double2 ds = *reinterpret_cast<const double2*>(sl + 64 + 2 * lane);
-    const double di0 = di.x, di1 = di.y;
-    const double2 ro = *reinterpret_cast<const double2*>(sl + kBStat16 + 2 * lane);
-    const double2 qo = *reinterpret_cast<const double2*>(sl + kBStat16 + 64 + 2 * lane);
-    const double2 po = *reinterpret_cast<const double2*>(sl + kBStat16 + 128 + 2 * lane);
-    const double2 xo = *reinterpret_cast<const double2*>(sl + kBStat16 + kBDyn + 2 * lane);
-    const double r0 = __fma_rn(-c.a, qo.x, ro.x), r1n = __fma_rn(-c.a, qo.y, ro.y);
-    const double p0 = __fma_rn(di0, r0, __dmul_rn(c.b, po.x)), p1 = __fma_rn(di1, r1n, __dmul_rn(c.b, po.y));
-    __syncwarp();                                                 // previous chunk's pnb reads done
-    *reinterpret_cast<double2*>(pnb + 2 * lane) = make_double2(p0, p1);
-    __syncwarp();
-    const double f00 = far_pn16(g00, c.a, c.b), f01 = far_pn16(g01, c.a, c.b);
-    const double f10 = far_pn16(g10, c.a, c.b), f11 = far_pn16(g11, c.a, c.b);
-    auto nbv = [&](unsigned u, double far, double own) {
-      return none(u) ? own : ((u >> 8) == 127u ? pnb[u & 63u] : far);
-    };
-    double f02 = 0.0, f03 = 0.0, f12 = 0.0, f13 = 0.0;
-    if (__any_sync(0xffffffffu, isfar(u02) | isfar(u03) | isfar(u12) | isfar(u13))) {   // rare: > 2 far in a row
-      const FarRaw g02 = far_load16(dyns, stat, m, u02, isfar(u02)), g03 = far_load16(dyns, stat, m, u03, isfar(u03));
-      const FarRaw g12 = far_load16(dyns, stat, m, u12, isfar(u12)), g13 = far_load16(dyns, stat, m, u13, isfar(u13));
-      f02 = far_pn16(g02, c.a, c.b);
-      f03 = far_pn16(g03, c.a, c.b);
-      f12 = far_pn16(g12, c.a, c.b);
-      f13 = far_pn16(g13, c.a, c.b);
-    }
-    double s0 = p0 - nbv(u00, f00, p0);
-    s0 += p0 - nbv(u01, f01, p0);
-    s0 += p0 - nbv(u02, f02, p0);
-    s0 += p0 - nbv(u03, f03, p0);
-    double s1 = p1 - nbv(u10, f10, p1);
-    s1 += p1 - nbv(u11, f11, p1);
-    s1 += p1 - nbv(u12, f12, p1);
-    s1 += p1 - nbv(u13, f13, p1);
-    const double q0 = __fma_rn(T, s0, __dmul_rn(ds.x, p0));
-    const double q1 = __fma_rn(T, s1, __dmul_rn(ds.y, p1));
-    const int base = 64 * m + 2 * lane;
-    double* dd = dynd + (int64_t)m * kBDyn + 2 * lane;
-    st2mut(dd, make_double2(r0, r1n));
-    st2mut(dd + 64, make_double2(q0, q1));
-    st2mut(dd + 128, make_double2(p0, p1));
-    const double2 xn = make_double2(__fma_rn(c.a, po.x, xo.x), __fma_rn(c.a, po.y, xo.y));
-    if (base + 1 < r1) {
-      *reinterpret_cast<double2*>(xg + base) = xn;
-      c.accum(acc, p0, r0, di0, q0);
-      c.accum(acc, p1, r1n, di1, q1);
-    } else if (base < r1) {
-      xg[base] = xn.x;
-      c.accum(acc, p0, r0, di0, q0);
-    }
-  }
-}
-
 // Resident variant for latency-bound graphs (every warp owns <= kStages chunks,
 // DESIGN.md §5.3): the chunks' r, q, p, x, D^-1, shift and codes stay in this warp's
 // slots for the whole solve, so an iteration streams nothing; in-chunk neighbours read
@@ -2199,10 +2068,7 @@ __device__ void run_group(const StepParams& P, int g, int cl, double* x, const d
           if (P.cont[k].resident) {
             if (!CPL && P.cont[k].bstat) iter_ells_res2(c, P.cont[k], wg, W, st, j == 0, s, a5);
             else iter_ells_res<CPL>(c, P.cont[k], wg, W, st, j == 0, a5);
-          } else if (!CPL && P.cont[k].bdyn[0]) {
-            if (P.cont[k].bstat16) iter_ellb16(c, P.cont[k], wg, W, st, s, a5);
-            else iter_ellb(c, P.cont[k], wg, W, st, s, a5);
-          }
+          } else if (!CPL && P.cont[k].bdyn[0]) iter_ellb(c, P.cont[k], wg, W, st, s, a5);
           else iter_ells<CPL>(c, P.cont[k], wg, W, st, a5);
         }
       for (int it = ib + wg; it < ie; it += W) {

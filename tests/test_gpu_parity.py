@@ -145,13 +145,11 @@ def test_config1_streaming_jacobi_ell_pass(torch_cuda):
     assert reps[1]["iters"][1] > 10000
 
 
-@pytest.mark.parametrize("env", [{}, {"MC_COMPACT": "0"}, {"MC_BLOCKED": "0"}])
+@pytest.mark.parametrize("env", [{}, {"MC_BLOCKED": "0"}])
 def test_streaming_pass_variants(torch_cuda, env):
-    """The three streaming passes of a decoupled Jacobi solve on a fracture network -- the
-    compact chunk-blocked pass (default: uint16 codes, 88 B per row), the blocked pass with
-    int32 codes (MC_COMPACT=0: the fallback when a neighbour lies more than 127 chunks away,
-    96 B per row) and the pass on separate r, q, p arrays (MC_BLOCKED=0; the coupled scheme's
-    pass) -- each against the oracle at 1e-9: config 1's recipe on a 256^2 grid with
+    """The two streaming passes of a decoupled Jacobi solve on a fracture network -- the
+    chunk-blocked pass (default) and the pass on separate r, q, p arrays (MC_BLOCKED=0; the
+    coupled scheme's pass) -- each against the oracle at 1e-9: config 1's recipe on a 256^2 grid with
     4 CTAs (132 chunks for 32 warps: every staging slot is refilled).  The pass is chosen at
     load time, so each variant runs in a fresh process."""
     import subprocess
