@@ -1142,8 +1142,13 @@ static Plan make_plan(const mc_ctx* c, int scheme) {
     return P;
   }
   bool all_large = true, hist = true;
+  // a solve that can keep every CTA busy (bandwidth- or chunk-latency-bound: >= 2 rows per
+  // thread on all CTAs) gains nothing from running beside another one -- the streams contend
+  // and the split is never exactly balanced (config 2: 426 ms concurrent, 379 ms in phases);
+  // only solves too small for the whole grid (config 1's fracture network: 143 CTAs) run
+  // concurrently with the rest
   for (int a = 0; a < L; ++a) {
-    if (c->hc[a].n < kLargeRows) all_large = false;
+    if (c->hc[a].n < kLargeRows && useful_ctas(c->hc[a]) < T) all_large = false;
     if (c->plan_iters[a] <= 0) hist = false;
   }
   int ctas[MC_MAX_CONTINUA] = {0};
