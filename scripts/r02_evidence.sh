@@ -1,5 +1,5 @@
 #!/bin/bash
-# Regenerates round 2's committed evidence under gpurun_out/$1 (copy what is judged to profiles/):
+# Regenerates the committed evidence (supersedes round 1's gpu_profiles.sh): under gpurun_out/$1 (copy what is judged to profiles/):
 #   gpurun --timeout 6000 -- 'bash scripts/r02_evidence.sh r02final'
 R=gpurun_out/${1:-r02final}
 mkdir -p $R
