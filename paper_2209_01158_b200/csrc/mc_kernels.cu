@@ -66,14 +66,6 @@ __device__ __forceinline__ double pnew(double ro, double qo, double po, double d
 __device__ __forceinline__ void st_rec(double* rec, double r, double q, double p, double d) {
   asm volatile("st.global.cg.v4.f64 [%0], {%1,%2,%3,%4};" ::"l"(rec), "d"(r), "d"(q), "d"(p), "d"(d) : "memory");
 }
-struct RecRaw {
-  double r, q, p, d;
-};
-__device__ __forceinline__ RecRaw ld_rec(const double* rec) {
-  RecRaw v;
-  asm volatile("ld.global.cg.v4.f64 {%0,%1,%2,%3}, [%4];" : "=d"(v.r), "=d"(v.q), "=d"(v.p), "=d"(v.d) : "l"(rec) : "memory");
-  return v;
-}
 __device__ __forceinline__ double pn_rec(const double* rec, double a, double b) {
   double r, q, p, d;
   asm volatile("ld.global.cg.v4.f64 {%0,%1,%2,%3}, [%4];" : "=d"(r), "=d"(q), "=d"(p), "=d"(d) : "l"(rec) : "memory");
@@ -970,7 +962,7 @@ __device__ void iter_ells_res(const Ctx& c, const ContDev& C, int wg, int W, con
 // the previous iteration's r, q, p in global memory, in-chunk neighbours read the new p
 // from the slot.  r, p, q are published to global every iteration; x at the end.
 __device__ void iter_ells_res2(const Ctx& c, const ContDev& C, int wg, int W, const Stage& st, bool first, int s,
-                               const RecRaw* pre, double (&acc)[kNPart]) {
+                               double (&acc)[kNPart]) {
   double* wsm = st.wsm;
   const int lane = threadIdx.x & 31;
   const int64_t off = C.off;
@@ -1001,17 +993,10 @@ __device__ void iter_ells_res2(const Ctx& c, const ContDev& C, int wg, int W, co
     const int4 c0 = *reinterpret_cast<const int4*>(sl + 128 + 4 * lane);
     const int4 c1 = *reinterpret_cast<const int4*>(sl + 128 + 4 * lane + 2);
     double f00 = 0.0, f01 = 0.0, f10 = 0.0, f11 = 0.0;
-    if (pre && t == 0) {          // the first chunk's far records were loaded right after the barrier
-      f00 = pnew(pre[0].r, pre[0].q, pre[0].p, pre[0].d, c.a, c.b);
-      f01 = pnew(pre[1].r, pre[1].q, pre[1].p, pre[1].d, c.a, c.b);
-      f10 = pnew(pre[2].r, pre[2].q, pre[2].p, pre[2].d, c.a, c.b);
-      f11 = pnew(pre[3].r, pre[3].q, pre[3].p, pre[3].d, c.a, c.b);
-    } else {
-      if (c0.x >= 0) f00 = pn_rec(recs + 4 * (int64_t)c0.x, c.a, c.b);
-      if (c0.y >= 0) f01 = pn_rec(recs + 4 * (int64_t)c0.y, c.a, c.b);
-      if (c1.x >= 0) f10 = pn_rec(recs + 4 * (int64_t)c1.x, c.a, c.b);
-      if (c1.y >= 0) f11 = pn_rec(recs + 4 * (int64_t)c1.y, c.a, c.b);
-    }
+    if (c0.x >= 0) f00 = pn_rec(recs + 4 * (int64_t)c0.x, c.a, c.b);
+    if (c0.y >= 0) f01 = pn_rec(recs + 4 * (int64_t)c0.y, c.a, c.b);
+    if (c1.x >= 0) f10 = pn_rec(recs + 4 * (int64_t)c1.x, c.a, c.b);
+    if (c1.y >= 0) f11 = pn_rec(recs + 4 * (int64_t)c1.y, c.a, c.b);
     const double2 di = *reinterpret_cast<const double2*>(sl + 2 * lane);
     const double2 ds = *reinterpret_cast<const double2*>(sl + 64 + 2 * lane);
     const double2 ro = *reinterpret_cast<const double2*>(sl + 256 + 2 * lane);
@@ -1290,15 +1275,10 @@ __device__ void zero_item(const StepParams& P, const Item& it, double* x) {
 // ---------------------------------------------------------------- group all-reduce + barrier
 // Deterministic: CTA partial = fixed-order warp/CTA tree; group total = fixed-order sum
 // over the group's CTAs, computed redundantly (identically) by every CTA of the group.
-struct NoHook {
-  __device__ __forceinline__ void operator()() const {}
-};
-// `after_barrier` runs in every thread once the group has arrived (all CTAs' stores of this
-// pass are visible), before the partials are fetched: loads issued there overlap the fetch.
-template <int NP, class Hook = NoHook>
+template <int NP>
 __device__ __forceinline__ void group_allreduce(const StepParams& P, int g, int cl,
                                                 unsigned long long& epoch, const double (&v)[NP],
-                                                double (&out)[NP], Hook after_barrier = Hook()) {
+                                                double (&out)[NP]) {
   __shared__ double sh[2][kWarps][kNPart];
   __shared__ double tot[kNPart];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -1319,7 +1299,6 @@ __device__ __forceinline__ void group_allreduce(const StepParams& P, int g, int 
     // bitwise the multi-CTA path's at G = 1.  sh is parity-buffered: one barrier.
     asm volatile("fence.proxy.async.global;" ::: "memory");
     __syncthreads();
-    after_barrier();
 #pragma unroll
     for (int k = 0; k < NP; ++k) {
       double s = 0.0;
@@ -1362,7 +1341,6 @@ __device__ __forceinline__ void group_allreduce(const StepParams& P, int g, int 
 #endif
   }
   __syncthreads();
-  after_barrier();
   PROF_T(td);
   if (w < NP) {
     double s = 0.0;
@@ -2075,13 +2053,6 @@ __device__ void run_group(const StepParams& P, int g, int cl, double* x, const d
     c.ds = CPL ? P.dsC : P.dsD;
     c.a = 0.0;
     c.b = 0.0;
-    RecRaw pre[4];
-    bool havepre = false;
-    int resk = -1;                                  // the group's resident network on blocked data, if any
-#ifndef MC_NOPRE                                    // dev, A/B: -DMC_NOPRE=1 gathers inside the pass only
-    for (int k = 0; k < P.L; ++k)
-      if (((G.cont_mask >> k) & 1) && P.cont[k].rr && P.cont[k].resident && P.cont[k].bstat && P.cont[k].rrec[0]) resk = k;
-#endif
     for (int64_t j = 0;; ++j) {
       const int s = (int)(j & 1);
       c.rs = P.r[s];
@@ -2095,7 +2066,7 @@ __device__ void run_group(const StepParams& P, int g, int cl, double* x, const d
       for (int k = 0; k < P.L; ++k)
         if (((G.cont_mask >> k) & 1) && P.cont[k].rr) {
           if (P.cont[k].resident) {
-            if (!CPL && P.cont[k].bstat) iter_ells_res2(c, P.cont[k], wg, W, st, j == 0, s, havepre ? pre : nullptr, a5);
+            if (!CPL && P.cont[k].bstat) iter_ells_res2(c, P.cont[k], wg, W, st, j == 0, s, a5);
             else iter_ells_res<CPL>(c, P.cont[k], wg, W, st, j == 0, a5);
           } else if (!CPL && P.cont[k].bdyn[0]) iter_ellb(c, P.cont[k], wg, W, st, s, a5);
           else iter_ells<CPL>(c, P.cont[k], wg, W, st, a5);
@@ -2120,28 +2091,7 @@ __device__ void run_group(const StepParams& P, int g, int cl, double* x, const d
         PROF_ADD(g, 4, 1);
       }
 #endif
-      // resident network: the far records the NEXT pass needs for this warp's first chunk are
-      // loaded as soon as the group has arrived, overlapping the fetch of the partials
-      havepre = false;
-      if (!CPL && resk >= 0) {                      // uniform over the group: one instantiation per CTA
-        const ContDev& RC = P.cont[resk];
-        const double* recn = RC.rrec[s ^ 1];
-        const bool mine = wg < (int)((RC.n + 63) / 64);
-        group_allreduce<kNPart>(P, g, cl, epoch, a5, t5, [&]() {
-          if (mine) {
-            const int4* cds = reinterpret_cast<const int4*>(wsm + 128) + 2 * (threadIdx.x & 31);
-            const int4 c0 = cds[0], c1 = cds[1];
-            pre[0] = pre[1] = pre[2] = pre[3] = RecRaw{0.0, 0.0, 0.0, 0.0};
-            if (c0.x >= 0) pre[0] = ld_rec(recn + 4 * (int64_t)c0.x);
-            if (c0.y >= 0) pre[1] = ld_rec(recn + 4 * (int64_t)c0.y);
-            if (c1.x >= 0) pre[2] = ld_rec(recn + 4 * (int64_t)c1.x);
-            if (c1.y >= 0) pre[3] = ld_rec(recn + 4 * (int64_t)c1.y);
-          }
-        });
-        havepre = mine;
-      } else {
-        group_allreduce<kNPart>(P, g, cl, epoch, a5, t5);
-      }
+      group_allreduce<kNPart>(P, g, cl, epoch, a5, t5);
       passes = j + 1;
       rr = t5[1];
       if (j > 0 && rr <= G.tol2 * bb) {
