@@ -1119,15 +1119,29 @@ __device__ void iter_graph8(const Ctx& c, const ContDev& C, int r0, int r1,
   // neighbour gathers, so a row costs ~3 memory trips however long it is (<= 32 entries
   // per list in one batch; longer lists loop)
   const int lane = threadIdx.x & 31, sub = lane & 7, grp = lane >> 3;
+  // the row pointers of a batch are loaded one batch ahead, so a batch costs two memory
+  // trips (entries, then neighbour gathers) instead of three
+  int32_t e0 = 0, e1 = 0, f0 = 0, f1 = 0;
+  if (r0 + grp < r1) {
+    e0 = ldro(C.rowptr + r0 + grp);
+    e1 = ldro(C.rowptr + r0 + grp + 1);
+    if (CPL) {
+      f0 = ldro(c.P->cptr + C.off + r0 + grp);
+      f1 = ldro(c.P->cptr + C.off + r0 + grp + 1);
+    }
+  }
   for (int base = r0; base < r1; base += 4) {
     const int i = base + grp;
     const bool ok = i < r1;
     const int64_t gi = C.off + (ok ? i : r0);
-    const int32_t e0 = ok ? ldro(C.rowptr + i) : 0, e1 = ok ? ldro(C.rowptr + i + 1) : 0;
-    int32_t f0 = 0, f1 = 0;
-    if (CPL && ok) {
-      f0 = ldro(c.P->cptr + gi);
-      f1 = ldro(c.P->cptr + gi + 1);
+    int32_t e0n = 0, e1n = 0, f0n = 0, f1n = 0;
+    if (i + 4 < r1) {
+      e0n = ldro(C.rowptr + i + 4);
+      e1n = ldro(C.rowptr + i + 5);
+      if (CPL) {
+        f0n = ldro(c.P->cptr + gi + 4);
+        f1n = ldro(c.P->cptr + gi + 5);
+      }
     }
     double pc = 0.0, rc = 0.0, dc = 0.0;
     if (ok && sub == 0) c.own(gi, pc, rc, dc);
@@ -1175,6 +1189,10 @@ __device__ void iter_graph8(const Ctx& c, const ContDev& C, int r0, int r1,
       stmut(c.qd + gi, qv);
       c.accum(acc, pc, rc, dc, qv);
     }
+    e0 = e0n;
+    e1 = e1n;
+    f0 = f0n;
+    f1 = f1n;
   }
 }
 
