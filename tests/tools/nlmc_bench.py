@@ -1,13 +1,13 @@
 """NLMC space build on the GPU (mc_nlmc_build) for the paper-analogue scenarios, with the
 coarse solve of each scheme, and the oracle build timed beside it (one case, CPU).
-    python scripts/nlmc_bench.py [--oracle] [--out FILE]"""
+    python tests/tools/nlmc_bench.py [--oracle] [--out FILE]"""
 import argparse
 import json
 import os
 import sys
 import time
 
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 import numpy as np
 import torch
 
