@@ -111,12 +111,12 @@ def row_bytes(kind, path, nnz_off):
       streamed ELL chunks  read x, r, q, p, D^-1, shift (48) + 4 int32 codes (16) + write 32 = 96
       CSR rows             read 48 + row pointer 4 + 4 (col) or 12 (col + T) per entry + write 32
       resident ELL         the network's state stays in shared memory: only r, p, q are
-                           published for the other warps' gathers (24)
+                           published for the other warps' gathers, as one 32-byte record per row (32)
       block-Jacobi         resident: z, p published (16); streaming two-pass: 72 + 56 = 128
     Neighbour gathers are cache hits and are not counted."""
     if kind == "grid":
         return 96.0
-    return {0: 84.0 + nnz_off, 1: 96.0, 2: 24.0, 3: 16.0, 4: 128.0}[path]
+    return {0: 84.0 + nnz_off, 1: 96.0, 2: 32.0, 3: 16.0, 4: 128.0}[path]
 
 
 def step_bytes(pb, rep, scheme):
