@@ -121,6 +121,17 @@ struct Ctx {
     }
     return acc;
   }
+  // the same sum with the row's entry range [e0, e1) already loaded (grid strips load the
+  // range before they wait for the staged row, so the first of the three dependent trips
+  // -- range, entry, neighbour -- is off the critical path)
+  __device__ __forceinline__ double couple_q_range(int32_t e0, int32_t e1, double pc) const {
+    double acc = 0.0;
+    for (int32_t e = e0; e < e1; ++e) {
+      const int32_t j = ldro(P->cidx + e);
+      acc += ldro(P->cval + e) * (pc - pn_at(j));
+    }
+    return acc;
+  }
   __device__ __forceinline__ void accum(double (&acc)[kNPart], double pc, double rc, double dc,
                                         double qv) const {
     acc[0] += pc * qv;        // p.q
@@ -457,6 +468,13 @@ __device__ void iter_grid2s(const Ctx& c, const ContDev& C, int x0, int y0, int 
   }
   for (int y = y0; y < y1; ++y) {
     if (y + kStages - 1 < y1) prefetch(y + kStages - 1);
+    int32_t ce0 = 0, ce1 = 0, ce2 = 0;                             // coupled: entry ranges of this lane's two cells
+    if (CPL && valid) {
+      const int32_t* cp = c.P->cptr + off + (int64_t)y * nx + c0;
+      ce0 = ldro(cp);
+      ce1 = ldro(cp + 1);
+      ce2 = ldro(cp + 2);
+    }
 #if MC_TMA
     st.wait(y % kStages);
 #else
@@ -513,8 +531,8 @@ __device__ void iter_grid2s(const Ctx& c, const ContDev& C, int x0, int y0, int 
       q1 += ty.y * (pc.y - nxt.p.y);
       q1 += tym.y * (pc.y - pm.y);
       if (CPL) {
-        q0 += c.couple_q(gi, pc.x);
-        q1 += c.couple_q(gi + 1, pc.y);
+        q0 += c.couple_q_range(ce0, ce1, pc.x);
+        q1 += c.couple_q_range(ce1, ce2, pc.y);
       }
       st2mut(c.qd + gi, make_double2(q0, q1));
       c.accum(acc, pc.x, cur.r.x, cur.d.x, q0);
