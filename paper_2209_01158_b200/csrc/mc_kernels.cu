@@ -647,6 +647,16 @@ __device__ void iter_ells(const Ctx& c, const ContDev& C, int wg, int W, const S
   prefetch(wg);
   for (int m = wg; m < nch; m += W) {
     if (m + W < nch) prefetch(m + W);                             // next chunk in flight
+    int32_t ce0 = 0, ce1 = 0, ce2 = 0;                             // coupled: transfer entry ranges of this lane's two rows,
+    if (CPL) {                                                    // loaded before the wait for the staged chunk
+      const int64_t gr = off + 64 * (int64_t)m + 2 * lane;
+      if (64 * m + 2 * lane < r1) {
+        ce0 = ldro(c.P->cptr + gr);
+        ce1 = ldro(c.P->cptr + gr + 1);
+      }
+      ce2 = ce1;
+      if (64 * m + 2 * lane + 1 < r1) ce2 = ldro(c.P->cptr + gr + 2);
+    }
     st.wait(tix(m));
     const FarG fcur = far_gather(c, slot(m), lane);
     // stage C: chunk m
@@ -706,7 +716,7 @@ __device__ void iter_ells(const Ctx& c, const ContDev& C, int wg, int W, const S
         s += pc[h] - v;
       }
       qv[h] = sl[336 + 2 * lane + h] * pc[h] + C.Tconst * s;
-      if (CPL && base + h < r1) qv[h] += c.couple_q(g + h, pc[h]);
+      if (CPL && base + h < r1) qv[h] += c.couple_q_range(h == 0 ? ce0 : ce1, h == 0 ? ce1 : ce2, pc[h]);
     }
     if (ok1) st2mut(c.qd + g, make_double2(qv[0], qv[1]));
     else if (ok0) stmut(c.qd + g, qv[0]);
