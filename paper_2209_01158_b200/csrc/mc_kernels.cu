@@ -1728,34 +1728,38 @@ __device__ void bjs_pass_u(const StepParams& P, const ContDev& C, int wg, int W,
     const int base = 64 * m + 2 * lane;
     const int64_t g = off + base;
     double rn[2], xn[2];
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      const int l2 = 2 * lane + h;
-      xn[h] = __fma_rn(alpha, sl[128 + l2], sl[192 + l2]);
-      rn[h] = __fma_rn(-alpha, sl[64 + l2], sl[0 + l2]);
+    {
+      const double2 r2 = *reinterpret_cast<const double2*>(sl + 2 * lane);
+      const double2 q2 = *reinterpret_cast<const double2*>(sl + 64 + 2 * lane);
+      const double2 p2 = *reinterpret_cast<const double2*>(sl + 128 + 2 * lane);
+      const double2 x2 = *reinterpret_cast<const double2*>(sl + 192 + 2 * lane);
+      xn[0] = __fma_rn(alpha, p2.x, x2.x);
+      xn[1] = __fma_rn(alpha, p2.y, x2.y);
+      rn[0] = __fma_rn(-alpha, q2.x, r2.x);
+      rn[1] = __fma_rn(-alpha, q2.y, r2.y);
     }
     __syncwarp();
-    sl[2 * lane] = rn[0];
-    sl[2 * lane + 1] = rn[1];
+    *reinterpret_cast<double2*>(sl + 2 * lane) = make_double2(rn[0], rn[1]);
     __syncwarp();
-    {                                                   // z = M^{-1} r over the chunk
-      double z0, z1;
-      bj_scan_solve(sl, sl + 256, nullptr, sl + 384, lane, z0, z1);
-      sl[448 + 2 * lane] = z0;
-      sl[449 + 2 * lane] = z1;
+    double z0, z1;                                      // z = M^{-1} r over the chunk
+    bj_scan_solve(sl, sl + 256, nullptr, sl + 384, lane, z0, z1);
+    if (base + 1 < r1) {
+      *reinterpret_cast<double2*>(x + g) = make_double2(xn[0], xn[1]);
+      st2mut(P.r[0] + g, make_double2(rn[0], rn[1]));
+      st2mut(zg + g, make_double2(z0, z1));
+      if (pzero) st2mut(pzero + g, make_double2(0.0, 0.0));
+      a2[0] += rn[0] * z0;
+      a2[1] += rn[0] * rn[0];
+      a2[0] += rn[1] * z1;
+      a2[1] += rn[1] * rn[1];
+    } else if (base < r1) {
+      x[g] = xn[0];
+      stmut(P.r[0] + g, rn[0]);
+      stmut(zg + g, z0);
+      if (pzero) stmut(pzero + g, 0.0);
+      a2[0] += rn[0] * z0;
+      a2[1] += rn[0] * rn[0];
     }
-    __syncwarp();
-#pragma unroll
-    for (int h = 0; h < 2; ++h)
-      if (base + h < r1) {
-        const double zv = sl[448 + 2 * lane + h];
-        x[g + h] = xn[h];
-        stmut(P.r[0] + g + h, rn[h]);
-        stmut(zg + g + h, zv);
-        if (pzero) stmut(pzero + g + h, 0.0);
-        a2[0] += rn[h] * zv;
-        a2[1] += rn[h] * rn[h];
-      }
   }
 }
 
