@@ -22,6 +22,10 @@ flux_pcg.c / fluxcg
           sparse factorisation cannot take (configs 2 and 4); the
           C library is compiled on first use (gcc) or by __graft_entry__.build().
 
+nlmc      the NLMC multiscale space of PAPER.md §4.1: bases of Eq. eq:basis per oversampled
+          region (KKT systems, SuperLU), R, the coarse system in flux form (readings
+          C30-C33), pinned by tests/test_nlmc_oracle.py.
+
 Every function is pinned by ``tests/test_oracle_*.py`` against closed forms,
 brute force and the paper's / SPEC's worked examples.
 """
